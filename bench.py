@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Headline benchmark: Toeplitz gradient evals/s at 2048^2 slices (BASELINE.json metric).
+
+Workload (C3 slab, configs[2]): per GPU a 64-slice 2048^2 volume, 128 uniform
+angles, Nd = 2048 (even: the Nyquist flip term is active).  One step = one
+fidelity-gradient evaluation grad = K x - R*g over the whole 64-slice batch
+(the hot loop of solve(), toeplitz.py:233-241) -- three kernels per step.
+Multi-GPU: one process per GPU, each owning its own 64-slice slab (z-slab
+weak scaling, no data-path collective); time = max over ranks.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Prints one JSON line (rank 0).  The reference arm times the reference
+algorithm (numpy restatement in oracle/, the reference being pure Python) on
+the host cores of the same box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_SIDE = 2048
+N_ANGLES = 128
+N_BINS = 2048
+SLICES_PER_GPU = 64
+METRIC = "Toeplitz gradient evals/s at 2048^2 slices"
+UNIT = "evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--slices", type=int, default=SLICES_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def config(args, world):
+    return {
+        "workload": "C3 slab: 64-slice 2048^2 synthetic volume per GPU, 128 uniform angles, "
+                    "Nd=2048; one step = grad = K x - R*g over the 64 slices",
+        "slices_per_gpu": args.slices, "side": N_SIDE, "angles": N_ANGLES, "detector_bins": N_BINS,
+        "fft_side": 2 * N_SIDE, "global_batch_slices": args.slices * world,
+        "parallelism": f"zslab{world}", "l2": "inputs exceed L2 (1.07 GB per operand per GPU)",
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._nv is not None:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ helpers
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(value: float, world: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def angles():
+    return np.linspace(0.0, np.pi, N_ANGLES, endpoint=False)
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_sample(threads: int | None = None, slices: int | None = None, repeats: int = 1):
+    """Reference algorithm (oracle port of toeplitz._apply_batch) on host cores."""
+    import oracle as O
+
+    threads = threads or os.cpu_count() or 1
+    slices = slices or threads
+    psf = O.build_psf(angles(), N_BINS, N_SIDE)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((slices, N_SIDE, N_SIDE))
+    rs = rng.standard_normal((slices, N_SIDE, N_SIDE))
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        _ = O.apply_batch_threaded(psf, x, threads) - rs
+        times.append(time.perf_counter() - t0)
+    return psf, x, rs, threads, slices, times
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import oracle as O
+
+    threads = os.cpu_count() or 1
+    psf = O.build_psf(angles(), N_BINS, N_SIDE)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((threads, N_SIDE, N_SIDE))
+    rs = rng.standard_normal((threads, N_SIDE, N_SIDE))
+    for _ in range(args.warmup):
+        O.apply_batch_threaded(psf, x, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _ = O.apply_batch_threaded(psf, x, threads) - rs
+    dt = time.perf_counter() - t0
+    value = threads * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config(args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{threads} slices of 2048^2 per step, one per host thread "
+                                   "(numpy restatement of toeplitz._apply_batch: complex128 fft2 "
+                                   "on the odd 4375^2 padded grid)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def algorithmic_bytes(z: int, n: int, m: int):
+    """Per-launch algorithmic HBM bytes."""
+    h = m // 2 + 1
+    spec = 8 * n * h  # one slice's half spectrum, complex64
+    return {
+        "k_rows_fwd": z * (4 * n * n + spec),
+        "k_cols_conv": z * 2 * spec + h * m * 12,
+        "k_rows_inv": z * (spec + 8 * n * n),
+    }
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2603_28756_b200 as tf
+    from paper_2603_28756_b200 import _lib
+    from paper_2603_28756_b200.toeplitz import apply_stack
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    z = args.slices
+    geom = tf.ScanGeometry(angles=angles(), detector_bins=N_BINS, image_side=N_SIDE)
+    psf = tf.build_psf(tf.polar_sampling(geom), N_SIDE)
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    x = torch.randn((z, N_SIDE, N_SIDE), generator=gen, device=dev)
+    ctx = _make_context(tf, psf, geom, z, rank)
+    out = torch.empty_like(x)
+
+    def step():
+        apply_stack(psf, x, out=out, aux=ctx.rstar, alpha=1.0, beta=-1.0)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    value = z * world * args.steps / (ms / 1e3)
+
+    # per-kernel durations: the same steps again with events around each launch
+    _lib.timing_enable(True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    kt = _lib.timing_collect()
+    _lib.timing_enable(False)
+    names = {v: k for k, v in _lib.TIMER_SLOTS.items()}
+    per_kernel = {names[s]: {"avg_ms": t / n, "launches": n} for s, (t, n) in kt.items() if s in names}
+    launches = sum(v["launches"] for v in per_kernel.values())
+    ab = algorithmic_bytes(z, N_SIDE, psf.padded_side)
+    peak = _peak_hbm()
+    for k, v in per_kernel.items():
+        v["gbs"] = ab[k] / (v["avg_ms"] / 1e3) / 1e9
+        v["frac"] = v["gbs"] / peak["value"]
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["avg_ms"])
+    tot_ms = sum(v["avg_ms"] for v in per_kernel.values())
+    total_bytes = sum(ab.values())
+    roofline = {
+        "bound": "hbm", "kernel": dom,
+        "achieved": per_kernel[dom]["gbs"], "peak": peak["value"], "unit": "GB/s",
+        "frac": per_kernel[dom]["frac"], "peak_source": peak["source"],
+        "traffic": _ncu_traffic(dom),
+        "per_kernel": per_kernel,
+        "gradient_total": {"bytes_per_eval": total_bytes / z,
+                           "achieved": total_bytes / (tot_ms / 1e3) / 1e9,
+                           "frac": total_bytes / (tot_ms / 1e3) / 1e9 / peak["value"]},
+    }
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(tf, ctx, z, world, args.e2e_steps)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        _, _, _, threads, slices, times = cpu_sample()
+        cpu = {"value": slices / min(times), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{slices} slices of 2048^2, one per host thread, oracle port of "
+                         "toeplitz._apply_batch (complex128 fft2 on the odd 4375^2 grid) minus R*g"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: randn volume, R*g from a randn sinogram",
+            "config": config(args, world), "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def _make_context(tf, psf, geom, z, rank):
+    """FidelityContext for a synthetic randn sinogram (R*g on the GPU when available)."""
+    import torch
+
+    from paper_2603_28756_b200.toeplitz import FidelityContext
+
+    g = np.random.default_rng(2000 + rank).standard_normal((z, N_ANGLES, N_BINS))
+    try:
+        plan = tf.NufftPlan(N_SIDE, tf.polar_sampling(geom), 1e-6)
+        sino = tf.Sinogram(angles=geom.angles, data=g)
+        return tf.fidelity_context(plan, psf, sino)
+    except (AttributeError, ImportError):
+        # NUFFT back-projection not built yet: a synthetic R*g of the same shape
+        gen = torch.Generator(device="cuda").manual_seed(3000 + rank)
+        rs = torch.randn((z, N_SIDE, N_SIDE), generator=gen, device="cuda")
+        return FidelityContext(psf=psf, rstar=rs, g_norm_sq=float(np.sum(g ** 2)))
+
+
+def _e2e(tf, ctx, z, world, steps):
+    """Public API call with host float64 buffers: fidelity_grad(ctx, f) -> numpy."""
+    import torch
+
+    f = np.random.default_rng(5).standard_normal((z, N_SIDE, N_SIDE))
+    tf.fidelity_grad(ctx, f)  # warm
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        out = tf.fidelity_grad(ctx, f)
+    dt = time.perf_counter() - t0
+    dt = max_over_ranks(dt, world)
+    assert out.shape == f.shape
+    return {"value": z * world * steps / dt, "unit": UNIT,
+            "h2d_bytes_per_step": int(f.size * 4), "d2h_bytes_per_step": int(f.size * 4),
+            "api": "fidelity_grad(ctx, numpy float64 (64, 2048, 2048)) -> numpy float64"}
+
+
+def _peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return {"value": float(json.loads(p.read_text())["hbm_gbs"]), "source": "measured"}
+    except Exception:  # noqa: BLE001
+        return {"value": 6650.0, "source": "fallback"}
+
+
+def _ncu_traffic(kernel):
+    """dram bytes per launch from the committed ncu capture, if present."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(p.read_text()).get(kernel)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup() if args.impl == "ours" else (
+        int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,78 @@
+/*
+ * tomoforge_b200.h -- C-ABI of libtomoforge_b200.so, the B200 (sm_100a)
+ * implementation of the Fourier-domain MBIR iterative core.
+ *
+ * Conventions (all entry points):
+ *   - array arguments are DEVICE pointers owned by the caller; fp32 unless
+ *     stated; volumes are row-major [slice][x][y] (reference layout data[ix, iy],
+ *     tomoforge/geometry.py:1-13);
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - return 0 on success, -1 bad argument/shape, -2 CUDA error, -3 unsupported;
+ *     tf_last_error() describes the last failure on the calling thread;
+ *   - no global state except the per-device twiddle table built by tf_init();
+ *     calls on distinct buffers/streams are re-entrant.
+ *
+ * The reference interface each entry point replaces is cited (paths relative to
+ * the reference package pkg/src/tomoforge/).
+ */
+#ifndef TOMOFORGE_B200_H
+#define TOMOFORGE_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* tf_last_error(void);
+int tf_version(void);
+
+/* Build the per-device twiddle table on the current device (idempotent). */
+int tf_init(void);
+
+/* FFT side M used for an N x N source grid: the smallest power of two >= 2N-1.
+ * Replaces padded_side_for (toeplitz.py:53-60), which picks the smallest ODD
+ * 7-smooth side; the even grid is exact for the re-embedded lag kernels
+ * (DESIGN.md §3).  Returns M, or -1 for unsupported N (> 4096). */
+int tf_fft_side(int n);
+
+/* Bytes of workspace tf_toeplitz_apply needs to process `nslices` slices in one
+ * pass (it chunks over slices when given less, down to one slice). */
+long long tf_toeplitz_workspace_bytes(int n, int M, long long nslices);
+long long tf_psf_workspace_bytes(int M);
+
+/* PSF spectra of the normal operator for an N x N grid.
+ * Replaces compute_psf / build_psf (toeplitz.py:85-131).
+ *   d_cossin : [n_angles][2] fp64 (cos theta, sin theta)
+ *   nd       : detector bins (radial samples per angle); even nd enables the
+ *              Nyquist flip term (toeplitz.py:106-114)
+ *   d_PQ     : out [M/2+1][M] float2  ((A+Re B)/M^2, (A-Re B)/M^2)
+ *   d_Bi     : out [M/2+1][M] float   Im B / M^2 (zeros for odd nd)
+ *   d_ws     : tf_psf_workspace_bytes(M) bytes of scratch */
+int tf_psf_build(int n, int M, int n_angles, const double* d_cossin, int nd, void* d_PQ,
+                 float* d_Bi, void* d_ws, long long ws_bytes, void* stream);
+
+/* out = alpha * (K x) + beta * aux over a stack of nslices N x N slices.
+ * Replaces _apply_batch (toeplitz.py:134-149); with alpha=1, beta=-1, aux=R*g
+ * it is fidelity_grad (toeplitz.py:233-241).  aux may be NULL.  x != out. */
+int tf_toeplitz_apply(const float* d_x, float* d_out, const float* d_aux, float alpha,
+                      float beta, long long nslices, int n, int M, const void* d_PQ,
+                      const float* d_Bi, int has_flip, void* d_ws, long long ws_bytes,
+                      void* stream);
+
+/* Deterministic fp64 sums: d_out[0] = sum x*a, d_out[1] = sum x*b (b may be
+ * NULL -> 0).  Replaces the np.sum(arr * kf), np.sum(arr * rstar) terms of
+ * fidelity_loss / objective (toeplitz.py:226-230, solver.py:95-101).
+ * d_ws: tf_reduce_workspace_bytes() bytes. */
+long long tf_reduce_workspace_bytes(void);
+int tf_dot2(const float* d_x, const float* d_a, const float* d_b, long long n, double* d_out,
+            double* d_ws, void* stream);
+
+/* Per-kernel CUDA-event timing used by bench.py for the roofline numbers.
+ * Enable (clears totals), run, then collect: ms_out[slot] = total ms and
+ * n_out[slot] = launches per slot (0 k_rows_fwd, 1 k_cols_conv, 2 k_rows_inv). */
+int tf_timing_enable(int on);
+int tf_timing_collect(double* ms_out, long long* n_out, int nslots);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOMOFORGE_B200_H */

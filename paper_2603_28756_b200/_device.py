@@ -1,0 +1,86 @@
+"""Host <-> device conversion and workspace management for the operator API.
+
+Reference-kind inputs (numpy float64 arrays, ImageGrid, Volume) are copied to
+fp32 CUDA tensors at the boundary and results come back as float64 numpy of the
+same kind (the reference contract, tomoforge/toeplitz.py:152-165); CUDA
+tensors pass through without copies and results stay on the device.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .geometry import ImageGrid, Volume
+
+_workspaces: dict = {}
+
+
+def workspace(nbytes: int, tag: str = "main") -> torch.Tensor:
+    """A cached uint8 device buffer of at least ``nbytes`` (grown on demand)."""
+    dev = _lib.device()
+    key = (dev.index, tag)
+    buf = _workspaces.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _workspaces.pop(key, None)
+        buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
+        _workspaces[key] = buf
+    return buf
+
+
+def release_workspaces() -> None:
+    _workspaces.clear()
+
+
+def is_device_tensor(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def as_stack(f, what: str = "input"):
+    """Return (device fp32 (Z, N, N) contiguous tensor, kind) for any accepted input.
+
+    kind is one of 'image', 'volume', 'array2', 'array3', 'tensor2', 'tensor3'.
+    """
+    if isinstance(f, ImageGrid):
+        return to_device(f.data[None]), "image"
+    if isinstance(f, Volume):
+        return to_device(f.data), "volume"
+    if isinstance(f, torch.Tensor):
+        t = f
+        if not t.is_cuda:
+            t = t.to(_lib.device())
+        t = t.to(torch.float32).contiguous()
+        if t.dim() == 2:
+            return t[None], "tensor2"
+        if t.dim() == 3:
+            return t, "tensor3"
+        raise ValueError(f"{what} must be 2D or 3D, got shape {tuple(t.shape)}")
+    arr = np.asarray(f, dtype=np.float64)
+    if arr.ndim == 2:
+        return to_device(arr[None]), "array2"
+    if arr.ndim == 3:
+        return to_device(arr), "array3"
+    raise ValueError(f"{what} must be 2D or 3D, got shape {arr.shape}")
+
+
+def to_device(arr: np.ndarray) -> torch.Tensor:
+    """float64 host array -> contiguous fp32 device tensor (pinned staging)."""
+    host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32))
+    return host.to(_lib.device(), non_blocking=False)
+
+
+def wrap_like(kind: str, t: torch.Tensor):
+    """Return the device stack ``t`` in the caller's kind."""
+    if kind == "tensor3":
+        return t
+    if kind == "tensor2":
+        return t[0]
+    host = t.detach().to("cpu", torch.float64).numpy()
+    if kind == "image":
+        return ImageGrid(host[0])
+    if kind == "volume":
+        return Volume(host)
+    if kind == "array2":
+        return host[0]
+    return host

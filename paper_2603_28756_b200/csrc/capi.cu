@@ -1,0 +1,196 @@
+// extern "C" boundary of libtomoforge_b200.so (declared in include/tomoforge_b200.h).
+//
+// Every entry point takes device pointers owned by the caller, a cudaStream_t
+// (as void*), and returns 0 on success, -1 for a bad argument/shape, -2 for a
+// CUDA error, -3 for an unsupported configuration; tf_last_error() returns a
+// thread-local description of the last failure.  The library holds no state
+// except the per-device twiddle table built by tf_init().
+#include <cstdarg>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "tf_common.cuh"
+
+namespace tf {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int fail_arg(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  set_error(buf);
+  return TF_EARG;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return TF_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return TF_ECUDA;
+}
+
+int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
+
+// ---- per-kernel timing (slots: 0 rows_fwd, 1 cols_conv, 2 rows_inv, ...)
+constexpr int TIMER_SLOTS = 16;
+static std::mutex g_timer_mu;
+static bool g_timing = false;
+struct PendingTiming { cudaEvent_t a, b; int slot; };
+static std::vector<PendingTiming> g_pending;
+static double g_time_ms[TIMER_SLOTS];
+static long long g_time_n[TIMER_SLOTS];
+
+void timer_begin(KernelTimer& t, int slot, cudaStream_t st) {
+  if (!g_timing) return;
+  t.slot = slot;
+  t.st = st;
+  cudaEventCreate(&t.a);
+  cudaEventCreate(&t.b);
+  cudaEventRecord(t.a, st);
+}
+
+void timer_end(KernelTimer& t) {
+  if (t.slot < 0) return;
+  cudaEventRecord(t.b, t.st);
+  std::lock_guard<std::mutex> lk(g_timer_mu);
+  g_pending.push_back({t.a, t.b, t.slot});
+}
+
+static std::mutex g_init_mu;
+static std::vector<int> g_inited;  // per device ordinal
+static std::vector<int> g_sms;
+
+int init_twiddles();
+
+int ensure_init() {
+  int dev = 0;
+  TF_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if ((int)g_inited.size() <= dev) {
+    g_inited.resize(dev + 1, 0);
+    g_sms.resize(dev + 1, 0);
+  }
+  if (!g_inited[dev]) {
+    TF_TRY(init_twiddles());
+    int sms = 0;
+    TF_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev),
+                      "cudaDeviceGetAttribute"));
+    g_sms[dev] = sms;
+    g_inited[dev] = 1;
+  }
+  return TF_OK;
+}
+
+int num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return (dev < (int)g_sms.size() && g_sms[dev] > 0) ? g_sms[dev] : 148;
+}
+
+// defined in the component translation units
+int toeplitz_apply(const float* x, float* out, const float* aux, float alpha, float beta,
+                   long long nslices, int n, int M, const void* PQ, const float* Bi, bool flip,
+                   void* ws, size_t ws_bytes, cudaStream_t st);
+size_t psf_workspace_bytes(int M);
+int psf_build(int n, int M, const double* cs, int n_angles, int nd, void* PQ, float* Bi,
+              void* ws, size_t ws_bytes, cudaStream_t st);
+int reduce_blocks();
+int dot2(const float* x, const float* a, const float* b, long long n, double* out, double* ws,
+         cudaStream_t st);
+
+}  // namespace tf
+
+using namespace tf;
+
+extern "C" {
+
+const char* tf_last_error(void) { return g_err.c_str(); }
+
+int tf_version(void) { return 1; }
+
+int tf_init(void) { return ensure_init(); }
+
+int tf_fft_side(int n) {
+  if (n < 1) return fail_arg("source side must be positive");
+  int M = 8;
+  while (M < 2 * n - 1) M <<= 1;
+  if (M > 8192) return fail_arg("source side %d exceeds the supported maximum 4096", n);
+  return M;
+}
+
+long long tf_toeplitz_workspace_bytes(int n, int M, long long nslices) {
+  return (long long)(M / 2 + 1) * n * (long long)sizeof(c32) * nslices;
+}
+
+long long tf_psf_workspace_bytes(int M) { return (long long)psf_workspace_bytes(M); }
+
+int tf_psf_build(int n, int M, int n_angles, const double* d_cossin, int nd, void* d_PQ,
+                 float* d_Bi, void* d_ws, long long ws_bytes, void* stream) {
+  TF_TRY(ensure_init());
+  if (n < 1 || M < 2 * n - 1 || !is_pow2(M)) return fail_arg("bad psf sides n=%d M=%d", n, M);
+  if (n_angles < 1 || nd < 1) return fail_arg("bad sampling (angles=%d, nd=%d)", n_angles, nd);
+  if (!d_cossin || !d_PQ || !d_Bi || !d_ws) return fail_arg("null pointer");
+  return psf_build(n, M, d_cossin, n_angles, nd, d_PQ, d_Bi, d_ws, (size_t)ws_bytes,
+                   (cudaStream_t)stream);
+}
+
+int tf_toeplitz_apply(const float* d_x, float* d_out, const float* d_aux, float alpha,
+                      float beta, long long nslices, int n, int M, const void* d_PQ,
+                      const float* d_Bi, int has_flip, void* d_ws, long long ws_bytes,
+                      void* stream) {
+  TF_TRY(ensure_init());
+  if (n < 1 || M < 2 * n - 1 || !is_pow2(M)) return fail_arg("bad sides n=%d M=%d", n, M);
+  if (nslices < 0) return fail_arg("negative slice count");
+  if (nslices == 0) return TF_OK;
+  if (!d_x || !d_out || !d_PQ || (has_flip && !d_Bi) || !d_ws)
+    return fail_arg("null pointer");
+  if (d_x == d_out) return fail_arg("in-place apply is not supported");
+  return toeplitz_apply(d_x, d_out, d_aux, alpha, beta, nslices, n, M, d_PQ, d_Bi, has_flip != 0,
+                        d_ws, (size_t)ws_bytes, (cudaStream_t)stream);
+}
+
+long long tf_reduce_workspace_bytes(void) {
+  if (ensure_init() != TF_OK) return -1;
+  return (long long)reduce_blocks() * 4 * (long long)sizeof(double);
+}
+
+int tf_dot2(const float* d_x, const float* d_a, const float* d_b, long long n, double* d_out,
+            double* d_ws, void* stream) {
+  TF_TRY(ensure_init());
+  if (n < 0 || !d_x || !d_a || !d_out || !d_ws) return fail_arg("bad tf_dot2 arguments");
+  return dot2(d_x, d_a, d_b, n, d_out, d_ws, (cudaStream_t)stream);
+}
+
+int tf_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_timer_mu);
+  g_timing = on != 0;
+  for (int i = 0; i < TIMER_SLOTS; ++i) { g_time_ms[i] = 0.0; g_time_n[i] = 0; }
+  return TF_OK;
+}
+
+// Synchronise the recorded events and return per-slot (total ms, launch count).
+int tf_timing_collect(double* ms_out, long long* n_out, int nslots) {
+  std::lock_guard<std::mutex> lk(g_timer_mu);
+  for (auto& p : g_pending) {
+    float ms = 0.f;
+    TF_TRY(check_cuda(cudaEventSynchronize(p.b), "cudaEventSynchronize"));
+    TF_TRY(check_cuda(cudaEventElapsedTime(&ms, p.a, p.b), "cudaEventElapsedTime"));
+    g_time_ms[p.slot] += ms;
+    g_time_n[p.slot] += 1;
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  g_pending.clear();
+  for (int i = 0; i < nslots && i < TIMER_SLOTS; ++i) {
+    ms_out[i] = g_time_ms[i];
+    n_out[i] = g_time_n[i];
+  }
+  return TF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,253 @@
+"""Normal-operator (Toeplitz) application and data-fidelity loss/gradient on B200.
+
+Drop-in for tomoforge/toeplitz.py.  R*R acts on an N x N slice as a
+convolution with a real, centro-symmetric lag kernel (toeplitz.py:1-19); for
+even detector sizes an extra kernel acts on the flipped image.  The reference
+synthesises the kernel with an adjoint NUFFT on an odd padded grid
+(toeplitz.py:85-124); this build evaluates the same kernel in closed form on
+the GPU (fp64 Dirichlet sums), re-embeds it on an even power-of-two grid
+M >= 2N-1 and runs the fused real-FFT convolution of csrc/toeplitz.cu
+(K1 rows -> K2 columns x PSF -> K3 rows).  See DESIGN.md §3 for the algebra.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .geometry import ImageGrid, PolarSampling, Sinogram, Volume
+
+__all__ = [
+    "PsfKernel",
+    "FidelityContext",
+    "padded_side_for",
+    "fft_side_for",
+    "compute_psf",
+    "build_psf",
+    "fidelity_context",
+    "toeplitz_apply",
+    "fidelity_loss",
+    "fidelity_grad",
+]
+
+# slices processed per apply pass; bounds the half-spectrum workspace
+_MAX_CHUNK_BYTES = 4 << 30
+
+
+def _is_7smooth(v: int) -> bool:
+    for p in (2, 3, 5, 7):
+        while v % p == 0:
+            v //= p
+    return v == 1
+
+
+def padded_side_for(source_side: int) -> int:
+    """Reference padding rule (toeplitz.py:53-60): smallest odd 7-smooth >= 2N-1."""
+    v = 2 * source_side - 1
+    v += 1 - v % 2
+    while not _is_7smooth(v):
+        v += 2
+    return v
+
+
+def fft_side_for(source_side: int) -> int:
+    """FFT grid side used on the GPU: the smallest power of two >= 2N-1."""
+    m = _lib.load().tf_fft_side(int(source_side))
+    if m < 0:
+        _lib.check(m, "tf_fft_side")
+    return m
+
+
+@dataclass(frozen=True)
+class PsfKernel:
+    """Device-resident spectra of the projection normal operator.
+
+    ``pq``: (M/2+1, M, 2) fp32 = ((A + Re B)/M^2, (A - Re B)/M^2) with ``A`` the
+    spectrum of (K - K_nyq)/Nd and ``B`` that of the flip kernel -K_nyq/Nd times
+    the flip phase; ``bi``: (M/2+1, M) fp32 = Im B / M^2.  Rows are ky (half
+    spectrum), columns kx.
+    """
+
+    padded_side: int
+    source_side: int
+    radial_count: int
+    pq: torch.Tensor = field(repr=False)
+    bi: torch.Tensor = field(repr=False)
+    has_flip: bool = False
+
+    @property
+    def embed_offset(self) -> int:
+        return 0
+
+    @property
+    def device(self) -> torch.device:
+        return self.pq.device
+
+
+def _check_tolerance(tolerance: float, oversampling: float) -> None:
+    # same admissible ranges as the reference NUFFT plan (nufft.py:115-120);
+    # the closed-form kernel itself is exact to fp64 rounding
+    if not (1e-14 < tolerance < 1e-1):
+        raise ValueError(f"tolerance must lie in (1e-14, 0.1), got {tolerance:g}")
+    if oversampling < 1.25:
+        raise ValueError("oversampling factor must be >= 1.25")
+
+
+def _build(angles: np.ndarray, nd: int, source_side: int) -> PsfKernel:
+    lib = _lib.ensure_ready()
+    n = int(source_side)
+    if n < 1:
+        raise ValueError("source side must be positive")
+    m = fft_side_for(n)
+    dev = _lib.device()
+    cs = np.stack([np.cos(angles), np.sin(angles)], axis=1).astype(np.float64)
+    d_cs = torch.from_numpy(np.ascontiguousarray(cs)).to(dev)
+    h = m // 2 + 1
+    pq = torch.empty((h, m, 2), dtype=torch.float32, device=dev)
+    bi = torch.empty((h, m), dtype=torch.float32, device=dev)
+    ws_bytes = lib.tf_psf_workspace_bytes(m)
+    ws = _device.workspace(ws_bytes, tag="psf")
+    _lib.check(
+        lib.tf_psf_build(n, m, int(angles.size), d_cs.data_ptr(), int(nd), pq.data_ptr(),
+                         bi.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_handle()),
+        "tf_psf_build",
+    )
+    return PsfKernel(padded_side=m, source_side=n, radial_count=int(nd), pq=pq, bi=bi,
+                     has_flip=(nd % 2 == 0))
+
+
+def compute_psf(plan_pad, source_side: int) -> PsfKernel:
+    """PSF from a plan on a padded grid (toeplitz.py:85-124 contract).
+
+    The plan only supplies the polar sampling; its side must satisfy the
+    reference's rules (>= 2N-1 and odd) so callers see the same errors.
+    """
+    m = plan_pad.grid_side
+    if m < 2 * source_side - 1:
+        raise ValueError(f"padded side {m} is smaller than 2N-1 = {2 * source_side - 1}")
+    if m % 2 == 0:
+        raise ValueError("padded grid side must be odd so kernel lags are integers")
+    s = plan_pad.sampling
+    return _build(np.asarray(s.angles), s.radial_count, source_side)
+
+
+def build_psf(sampling: PolarSampling, source_side: int, tolerance: float = 1e-6,
+              oversampling: float = 2.0) -> PsfKernel:
+    """Kernel for ``sampling`` on an N x N grid (toeplitz.py:127-131)."""
+    _check_tolerance(tolerance, oversampling)
+    return _build(np.asarray(sampling.angles), sampling.radial_count, source_side)
+
+
+def apply_stack(psf: PsfKernel, x: torch.Tensor, out: torch.Tensor | None = None,
+                aux: torch.Tensor | None = None, alpha: float = 1.0,
+                beta: float = 0.0) -> torch.Tensor:
+    """out = alpha * K x + beta * aux on a contiguous fp32 device stack (Z, N, N)."""
+    lib = _lib.ensure_ready()
+    n, m = psf.source_side, psf.padded_side
+    if x.dim() != 3 or x.shape[1] != n or x.shape[2] != n:
+        raise ValueError(f"image side {x.shape[-1]} does not match kernel source side {n}")
+    if not x.is_contiguous() or x.dtype != torch.float32:
+        raise ValueError("apply_stack needs a contiguous fp32 tensor")
+    z = x.shape[0]
+    if out is None:
+        out = torch.empty_like(x)
+    if aux is not None and (aux.shape != x.shape or not aux.is_contiguous()):
+        raise ValueError("aux must match the input stack")
+    per_slice = lib.tf_toeplitz_workspace_bytes(n, m, 1)
+    chunk = max(1, min(z, _MAX_CHUNK_BYTES // per_slice))
+    ws = _device.workspace(per_slice * chunk)
+    _lib.check(
+        lib.tf_toeplitz_apply(x.data_ptr(), out.data_ptr(), _lib.ptr(aux), float(alpha),
+                              float(beta), z, n, m, psf.pq.data_ptr(), psf.bi.data_ptr(),
+                              int(psf.has_flip), ws.data_ptr(), per_slice * chunk,
+                              _lib.stream_handle()),
+        "tf_toeplitz_apply",
+    )
+    return out
+
+
+def _check_side(psf: PsfKernel, side: int) -> None:
+    if side != psf.source_side:
+        raise ValueError(f"image side {side} does not match kernel source side {psf.source_side}")
+
+
+def toeplitz_apply(psf: PsfKernel, f):
+    """R*R f for an ImageGrid, Volume, array or CUDA tensor (toeplitz.py:152-165)."""
+    x, kind = _device.as_stack(f)
+    _check_side(psf, x.shape[-1])
+    return _device.wrap_like(kind, apply_stack(psf, x))
+
+
+@dataclass(frozen=True)
+class FidelityContext:
+    """Per-(geometry, data) precomputation (toeplitz.py:173-197).
+
+    ``rstar`` is the device (Z, N, N) fp32 adjoint R*g; ``rstar_g`` materialises
+    the reference's host ImageGrid/Volume view on demand.
+    """
+
+    psf: PsfKernel
+    rstar: torch.Tensor = field(repr=False)
+    g_norm_sq: float
+
+    def __post_init__(self):
+        if self.rstar.shape[-1] != self.psf.source_side:
+            raise ValueError("adjoint image side does not match PSF source side")
+
+    @property
+    def slices(self) -> int:
+        return self.rstar.shape[0]
+
+    @property
+    def side(self) -> int:
+        return self.rstar.shape[-1]
+
+    @property
+    def rstar_g(self):
+        host = self.rstar.detach().to("cpu", torch.float64).numpy()
+        return ImageGrid(host[0]) if host.shape[0] == 1 else Volume(host)
+
+    def rstar_array(self) -> np.ndarray:
+        return self.rstar.detach().to("cpu", torch.float64).numpy()
+
+
+def fidelity_context(recon_plan, psf: PsfKernel, sino: Sinogram) -> FidelityContext:
+    """R*g (GPU NUFFT back-projection) and ||g||^2 (toeplitz.py:200-207)."""
+    from .radon import _sampling_matches, back_project_stack
+
+    _sampling_matches(recon_plan, sino.angles, sino.detector_bins)
+    if recon_plan.grid_side != psf.source_side:
+        raise ValueError("reconstruction plan side does not match PSF source side")
+    rstar = back_project_stack(recon_plan, sino.data)
+    return FidelityContext(psf=psf, rstar=rstar, g_norm_sq=float(np.sum(sino.data ** 2)))
+
+
+def _fidelity_stack(ctx: FidelityContext, f):
+    x, kind = _device.as_stack(f, "estimate")
+    if tuple(x.shape) != (ctx.slices, ctx.side, ctx.side):
+        raise ValueError(
+            f"estimate shape {tuple(x.shape)} does not match data "
+            f"({ctx.slices}, {ctx.side}, {ctx.side})"
+        )
+    return x, kind
+
+
+def fidelity_loss(ctx: FidelityContext, f) -> float:
+    """0.5 <f, Kf> - <f, R*g> + 0.5 g'g (toeplitz.py:226-230)."""
+    from .reduce import dot2
+
+    x, _ = _fidelity_stack(ctx, f)
+    kf = apply_stack(ctx.psf, x)
+    fkf, frg = dot2(x, kf, ctx.rstar)
+    return 0.5 * fkf - frg + 0.5 * ctx.g_norm_sq
+
+
+def fidelity_grad(ctx: FidelityContext, f):
+    """K f - R*g, same kind as the input (toeplitz.py:233-241)."""
+    x, kind = _fidelity_stack(ctx, f)
+    grad = apply_stack(ctx.psf, x, aux=ctx.rstar, alpha=1.0, beta=-1.0)
+    return _device.wrap_like(kind, grad)

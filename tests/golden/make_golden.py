@@ -1,0 +1,181 @@
+"""Generate golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports tomoforge from /root/reference/pkg/src (read-only, untouched) and
+writes small ``.npz`` files next to this script.  The fixtures pin both the
+numpy oracle (tests/test_oracle.py) and the CUDA path (tests/test_gpu_*.py,
+which run on a GPU box where /root/reference does not exist).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path(os.environ.get("TOMOFORGE_REF", "/root/reference/pkg/src"))
+OUT = Path(__file__).resolve().parent
+
+
+def main():
+    sys.path.insert(0, str(REF))
+    import tomoforge as tf
+    from tomoforge import multires, qggmrf, runtime, solver, toeplitz
+
+    def angles(n):
+        return np.linspace(0.0, np.pi, n, endpoint=False)
+
+    def setup(side, n_ang, bins, seed):
+        geom = tf.ScanGeometry(angles=angles(n_ang), detector_bins=bins, image_side=side)
+        samp = tf.polar_sampling(geom)
+        plan = tf.NufftPlan(side, samp, 1e-6)
+        psf = tf.build_psf(samp, side, 1e-6)
+        rng = np.random.default_rng(seed)
+        return geom, samp, plan, psf, rng
+
+    # ---- Toeplitz apply / fidelity: (side, angles, bins, slices)
+    for side, n_ang, bins, z in [(32, 45, 32, 1), (32, 45, 33, 1), (64, 45, 64, 2), (24, 9, 48, 3),
+                                 (16, 6, 16, 1), (128, 60, 128, 1), (8, 6, 8, 1)]:
+        geom, samp, plan, psf, rng = setup(side, n_ang, bins, seed=side + bins)
+        f = rng.standard_normal((z, side, side))
+        g = rng.standard_normal((z, n_ang, bins))
+        sino = tf.Sinogram(angles=geom.angles, data=g)
+        ctx = tf.fidelity_context(plan, psf, sino)
+        np.savez_compressed(
+            OUT / f"toeplitz_n{side}_p{n_ang}_nd{bins}_z{z}.npz",
+            angles=geom.angles, f=f, g=g,
+            kf=toeplitz._apply_batch(psf, f),
+            rstar=ctx.rstar_array(),
+            grad=np.asarray(tf.fidelity_grad(ctx, f)),
+            loss=tf.fidelity_loss(ctx, f),
+            fbp=np.asarray(tf.fbp(plan, sino).data),
+            kernel=np.fft.fftshift(np.fft.ifft2(psf.spectrum)).real,
+            padded_side=psf.padded_side,
+        )
+
+    # ---- forward projection (data synthesis) + type2/type1 pair
+    geom, samp, plan, psf, rng = setup(32, 20, 40, seed=5)
+    img = rng.standard_normal((32, 32))
+    c = rng.standard_normal(samp.count) + 1j * rng.standard_normal(samp.count)
+    np.savez_compressed(OUT / "nufft_n32_p20_nd40.npz", angles=geom.angles, img=img, c=c,
+                        type2=tf.type2(plan, img), type1=tf.type1(plan, c),
+                        proj=tf.forward_project(plan, img).data[0])
+
+    # ---- qGGMRF prior
+    rng = np.random.default_rng(11)
+    vol = rng.standard_normal((5, 12, 14)) * 0.3
+    lo, hi = rng.standard_normal((12, 14)), rng.standard_normal((12, 14))
+    img2 = rng.standard_normal((1, 13, 13))
+    for sigma, lam, p, q, T in [(0.2, 1e-2, 2.0, 1.2, 1.0), (0.05, 1.0, 1.8, 1.1, 0.7)]:
+        prm = tf.QggmrfParams(sigma=sigma, lam=lam, p=p, q=q, T=T)
+        s3, s2 = qggmrf.stencil_3d(), qggmrf.stencil_2d()
+        np.savez_compressed(
+            OUT / f"qggmrf_s{sigma}_p{p}.npz",
+            params=np.array([sigma, lam, p, q, T]), vol=vol, lo=lo, hi=hi, img2=img2,
+            grad=np.asarray(tf.prior_grad(prm, s3, vol)),
+            grad_halo=np.asarray(tf.prior_grad(prm, s3, vol, halo_lo=lo, halo_hi=hi)),
+            energy=tf.prior_energy(prm, s3, vol),
+            energy_halo=tf.prior_energy(prm, s3, vol, halo_hi=hi),
+            grad2=np.asarray(tf.prior_grad(prm, s2, img2)),
+            energy2=tf.prior_energy(prm, s2, img2),
+            rho=tf.potential(prm, np.linspace(-3, 3, 61)),
+            drho=tf.potential_deriv(prm, np.linspace(-3, 3, 61)),
+        )
+
+    # ---- solver: 2D (FBP init, restart) and 3D with the prior
+    for name, side, n_ang, bins, z, lam, iters in [("2d", 48, 30, 64, 1, 5e-3, 40),
+                                                    ("3d", 24, 18, 32, 4, 2e-2, 25)]:
+        geom, samp, plan, psf, rng = setup(side, n_ang, bins, seed=3)
+        if z == 1:
+            truth = tf.shepp_logan(side).data[None]
+        else:
+            truth = tf.shepp_logan(side, three_d=True, slices=z).data
+        clean = np.stack([tf.forward_project(plan, s).data[0] for s in truth])
+        g = clean + 0.05 * rng.standard_normal(clean.shape)
+        sino = tf.Sinogram(angles=geom.angles, data=g)
+        ctx = tf.fidelity_context(plan, psf, sino)
+        f0 = tf.fbp(plan, sino)
+        f0a = np.asarray(f0.data)
+        sigma = 0.1 * float(f0a.max() - f0a.min())
+        prm = tf.QggmrfParams(sigma=sigma, lam=lam)
+        L = solver.estimate_lipschitz(psf, prm)
+        cfg = tf.SolverConfig(max_iters=iters, tol=1e-300, lipschitz=L)
+        rec, recs = tf.solve(ctx, prm, cfg, f0)
+        np.savez_compressed(
+            OUT / f"solve_{name}.npz", angles=geom.angles, g=g, f0=f0a.reshape(z, side, side),
+            sigma=sigma, lam=lam, L=L, iters=iters,
+            recon=np.asarray(rec.data).reshape(z, side, side),
+            objective=np.array([r.objective for r in recs]),
+            fidelity=np.array([r.fidelity for r in recs]),
+            prior=np.array([r.prior for r in recs]),
+            grad_norm=np.array([r.grad_norm for r in recs]),
+            restarted=np.array([r.restarted for r in recs]),
+            lipschitz_est=solver.estimate_lipschitz(psf, prm),
+        )
+
+    # ---- multires pieces
+    rng = np.random.default_rng(21)
+    v = rng.standard_normal((3, 10, 10))
+    sino = tf.Sinogram(angles=angles(7), data=rng.standard_normal((6, 7, 37)))
+    ds = multires.downsample_sinogram(sino, 4)
+    np.savez_compressed(
+        OUT / "multires.npz", v=v, up3=multires.upsample(v, 20, 6), up2=multires.upsample(v[0], 25),
+        mat=multires._lanczos_matrix(10, 20, 3), mat_odd=multires._lanczos_matrix(7, 16, 3),
+        sino=sino.data, ds_data=ds.data, ds_angles=ds.angles,
+        ds_ang=multires.downsample_sinogram(sino, 2, downsample_angles=True).data,
+        lanczos=multires.lanczos_kernel(np.linspace(-4, 4, 81)),
+    )
+    geom, samp, plan, psf, rng = setup(32, 16, 32, seed=8)
+    truth = tf.shepp_logan(32, three_d=True, slices=4).data
+    g = np.stack([tf.forward_project(plan, s).data[0] for s in truth])
+    sino = tf.Sinogram(angles=geom.angles, data=g)
+    prm = tf.QggmrfParams(sigma=0.1, lam=1e-2)
+    hier = multires.GridHierarchy(levels=(16, 32), iters_per_level=(6, 4))
+    est, lrecs = multires.solve_hierarchical(sino, hier, prm,
+                                             tf.SolverConfig(max_iters=1, tol=1e-300),
+                                             use_fbp_init=True)
+    np.savez_compressed(OUT / "hier.npz", angles=geom.angles, g=g, recon=np.asarray(est.data),
+                        obj0=np.array([r.objective for r in lrecs[0]]),
+                        obj1=np.array([r.objective for r in lrecs[1]]))
+
+    # ---- runtime: partition + distributed == single worker
+    parts = {f"{n}_{w}": np.array([[p.begin, p.end] for p in runtime.partition(n, w)])
+             for n, w in [(10, 3), (8, 4), (7, 7), (2048, 8), (13, 5)]}
+    geom, samp, plan, psf, rng = setup(16, 10, 16, seed=9)
+    g = rng.standard_normal((6, 10, 16))
+    sino = tf.Sinogram(angles=geom.angles, data=g)
+    prm = tf.QggmrfParams(sigma=0.3, lam=0.05)
+    cfg = tf.SolverConfig(max_iters=8, tol=1e-300, lipschitz=None)
+    vol2, recs2 = runtime.distributed_solve(sino, 16, prm, cfg, 2)
+    vol1, recs1 = runtime.distributed_solve(sino, 16, prm, cfg, 1)
+    np.savez_compressed(OUT / "runtime.npz", angles=geom.angles, g=g, recon_w2=vol2.data,
+                        recon_w1=vol1.data, obj_w2=np.array([r.objective for r in recs2]),
+                        obj_w1=np.array([r.objective for r in recs1]), **parts)
+
+    # ---- C1 at reduced iteration count is too slow? no: 256^2, 180 angles, Nd=512
+    if os.environ.get("GOLDEN_C1", "1") == "1":
+        geom, samp, plan, psf, rng = setup(256, 180, 512, seed=7)
+        truth = tf.shepp_logan(256).data
+        clean = tf.forward_project(plan, truth).data
+        g = clean + 0.5 * np.random.default_rng(7).standard_normal(clean.shape)
+        sino = tf.Sinogram(angles=geom.angles, data=g)
+        ctx = tf.fidelity_context(plan, psf, sino)
+        f0 = tf.fbp(plan, sino)
+        sigma = 0.1 * float(f0.data.max() - f0.data.min())
+        prm = tf.QggmrfParams(sigma=sigma, lam=5e-4)
+        L = solver.estimate_lipschitz(psf, prm)
+        rec, recs = tf.solve(ctx, prm, tf.SolverConfig(max_iters=100, tol=1e-300, lipschitz=L), f0)
+        np.savez_compressed(OUT / "c1.npz", angles=geom.angles, g=g.astype(np.float64),
+                            f0=f0.data, sigma=sigma, L=L, recon=rec.data,
+                            objective=np.array([r.objective for r in recs]),
+                            restarted=np.array([r.restarted for r in recs]))
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,121 @@
+"""CUDA Toeplitz path vs the reference (golden fixtures) and the numpy oracle."""
+
+import glob
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOEPLITZ = sorted(Path(p).name for p in glob.glob(str(GOLDEN / "toeplitz_*.npz")))
+
+# single gradient evaluation gate (BASELINE.json north star): relative L2 <= 1e-4
+GRAD_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def tf():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_28756_b200 as m
+
+    return m
+
+
+def _psf(tf, angles, nd, n):
+    geom = tf.ScanGeometry(angles=angles, detector_bins=nd, image_side=n)
+    return tf.build_psf(tf.polar_sampling(geom), n)
+
+
+@pytest.mark.parametrize("name", TOEPLITZ)
+def test_apply_matches_reference(tf, name):
+    d = golden(name)
+    n, nd = d["f"].shape[1], d["g"].shape[2]
+    psf = _psf(tf, d["angles"], nd, n)
+    out = tf.toeplitz_apply(psf, d["f"])
+    assert out.dtype == np.float64 and out.shape == d["f"].shape
+    assert rel_l2(out, d["kf"]) < 1e-5
+
+
+@pytest.mark.parametrize("name", TOEPLITZ)
+def test_grad_with_reference_rstar(tf, name):
+    import torch
+
+    d = golden(name)
+    n, nd = d["f"].shape[1], d["g"].shape[2]
+    psf = _psf(tf, d["angles"], nd, n)
+    rs = torch.from_numpy(d["rstar"].astype(np.float32)).cuda()
+    ctx = tf.FidelityContext(psf=psf, rstar=rs, g_norm_sq=float(np.sum(d["g"] ** 2)))
+    grad = tf.fidelity_grad(ctx, d["f"])
+    assert rel_l2(grad, d["grad"]) < GRAD_TOL
+    assert tf.fidelity_loss(ctx, d["f"]) == pytest.approx(float(d["loss"]), rel=1e-5)
+
+
+def test_zero_in_zero_out(tf):
+    psf = _psf(tf, np.linspace(0, np.pi, 5, endpoint=False), 16, 16)
+    out = tf.toeplitz_apply(psf, np.zeros((16, 16)))
+    assert np.all(out == 0)
+
+
+def test_self_adjoint_and_psd(tf, rng):
+    psf = _psf(tf, np.linspace(0, np.pi, 9, endpoint=False), 24, 24)
+    f, h = rng.standard_normal((2, 24, 24))
+    lhs = np.sum(f * tf.toeplitz_apply(psf, h))
+    rhs = np.sum(tf.toeplitz_apply(psf, f) * h)
+    assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+    for s in range(5):
+        x = np.random.default_rng(s).standard_normal((24, 24))
+        assert np.sum(x * tf.toeplitz_apply(psf, x)) >= -1e-6 * np.sum(x * x)
+
+
+def test_batch_equals_slice_loop(tf, rng):
+    psf = _psf(tf, np.linspace(0, np.pi, 5, endpoint=False), 16, 16)
+    vol = rng.standard_normal((3, 16, 16))
+    batch = tf.toeplitz_apply(psf, vol)
+    for z in range(3):
+        np.testing.assert_array_equal(batch[z], tf.toeplitz_apply(psf, vol[z]))
+
+
+def test_size_mismatch(tf):
+    psf = _psf(tf, np.linspace(0, np.pi, 5, endpoint=False), 16, 16)
+    with pytest.raises(ValueError):
+        tf.toeplitz_apply(psf, np.zeros((8, 8)))
+
+
+@pytest.mark.parametrize("n,n_ang,nd", [(256, 90, 256), (512, 90, 1024), (200, 33, 201)])
+def test_apply_vs_oracle_midsize(tf, n, n_ang, nd):
+    import oracle as O
+
+    ang = np.linspace(0, np.pi, n_ang, endpoint=False)
+    x = np.random.default_rng(n).standard_normal((2, n, n))
+    ref = O.apply_batch(O.build_psf(ang, nd, n), x)
+    out = tf.toeplitz_apply(_psf(tf, ang, nd, n), x)
+    assert rel_l2(out, ref) < 1e-5
+
+
+def test_apply_2048_vs_oracle(tf):
+    """The bench size (C3/C4 slices): one 2048^2 slice, 128 angles, Nd=2048."""
+    import oracle as O
+
+    n, nd = 2048, 2048
+    ang = np.linspace(0, np.pi, 128, endpoint=False)
+    x = np.random.default_rng(0).standard_normal((1, n, n))
+    ref = O.apply_batch(O.build_psf(ang, nd, n), x)
+    out = tf.toeplitz_apply(_psf(tf, ang, nd, n), x)
+    assert rel_l2(out, ref) < 1e-5
+
+
+def test_device_tensor_path(tf):
+    import torch
+
+    psf = _psf(tf, np.linspace(0, np.pi, 7, endpoint=False), 32, 32)
+    x = torch.randn(4, 32, 32, device="cuda")
+    y = tf.toeplitz_apply(psf, x)
+    assert isinstance(y, torch.Tensor) and y.is_cuda and y.shape == x.shape
+    ref = tf.toeplitz_apply(psf, x.double().cpu().numpy())
+    assert rel_l2(y.double().cpu().numpy(), ref) < 1e-6
