@@ -124,7 +124,8 @@ int tf_fft_side(int n) {
 }
 
 long long tf_toeplitz_workspace_bytes(int n, int M, long long nslices) {
-  return (long long)(M / 2 + 1) * n * (long long)sizeof(c32) * nslices;
+  // row-blocked half spectra: [nslices][ceil(n/4)][M/2+1][4] complex64
+  return (long long)(M / 2 + 1) * 4 * ((n + 3) / 4) * (long long)sizeof(c32) * nslices;
 }
 
 long long tf_psf_workspace_bytes(int M) { return (long long)psf_workspace_bytes(M); }

@@ -2,119 +2,125 @@
 //
 // A length-M transform is run by a *group* of T = M/E threads; thread t keeps
 // the E elements {t + T*m : m < E} in registers ("canonical layout").  Each
-// pass applies radix-R butterflies (R | E, R <= 16) to register-resident
-// data; between passes the group exchanges through a padded shared-memory
-// buffer (index i -> i + i/16 keeps every exchange at the 2-wavefront minimum
-// for 8-byte elements).  With the first radix possibly smaller than 16 and all
-// later ones equal to E, both the first pass's input set and the last pass's
-// output set of thread t are exactly its canonical set, which is what lets the
-// Toeplitz column kernel multiply by the PSF and start the inverse transform
-// without touching shared memory (see toeplitz.cu, k_cols_conv).
+// pass applies radix-R butterflies (R | E, R <= 16) to register-resident data;
+// between passes the group exchanges through a padded shared-memory buffer
+// (word i lives at i + i/16, which keeps every exchange at the 2-wavefront
+// minimum for 8-byte elements).  The first radix may be smaller than E, all
+// later ones equal E; then the first pass's input set and the last pass's
+// output set of thread t are both its canonical set, which lets the Toeplitz
+// column kernel multiply by the PSF and start the inverse transform without a
+// shared-memory round trip (toeplitz.cu, k_cols_conv).
 //
-// Forward transforms use e^{-2 pi i jk/M} (numpy.fft sign); INV uses the
-// conjugate and is unnormalised.  Twiddles come from a fp32 table of
-// e^{-2 pi i j/TW_MAX} built once per device in fp64 (tf_init), with powers
-// w^r formed by a log-depth product tree (error ~log2(R) ulp).
+// Zero-padding is exploited explicitly: ZIN = the upper half of the canonical
+// inputs (m >= E/2, i.e. indices >= M/2) is zero, HOUT = only the lower half of
+// the outputs is needed; the first/last butterflies are pruned accordingly.
+//
+// Forward = e^{-2 pi i jk/M} (numpy.fft sign); INV = conjugate, unnormalised.
+// Twiddles: fp32 table of e^{-2 pi i j/TW_MAX} built in fp64 once per device
+// (tf_init); powers w^r by a log-depth product tree (error ~log2 R ulp).
 #pragma once
 #include "tf_complex.cuh"
 
 namespace tf {
 
 constexpr int TW_MAX = 16384;  // largest supported transform length
+// Concatenated per-length tables: W_L^j = e^{-2 pi i j/L} at word (L - 2) + j for
+// L = 2, 4, ..., TW_MAX, so the twiddles of one pass are contiguous in k.
+constexpr int TW_WORDS = 2 * TW_MAX - 2;
 // defined once: the library is a single translation unit (lib.cu)
-__device__ c32 g_twiddle[TW_MAX];
+__device__ c32 g_twiddle[TW_WORDS];
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 __host__ __device__ constexpr int pad_idx(int i) { return i + (i >> 4); }
-// padded exchange-buffer stride per group, chosen == 4 (mod 16) so that
-// concurrently used group buffers start on different bank pairs
-__host__ __device__ constexpr int group_stride(int M) {
-  return pad_idx(M) + ((4 - (pad_idx(M) % 16)) + 16) % 16 + 16;
+// exchange-buffer stride (c32 words) for `groups` concurrent buffers: spaced by
+// 16/groups bank pairs so that cross-buffer accesses of 16/groups consecutive
+// words by one warp never collide
+__host__ __device__ constexpr int group_stride(int M, int groups) {
+  return pad_idx(M) + 16 + ((((groups >= 16 ? 0 : 16 / groups) - pad_idx(M)) % 16) + 16) % 16;
 }
 
-template <bool INV>
-__device__ __forceinline__ c32 tw_table(int j) {  // e^{-+2 pi i j / TW_MAX}
-  c32 w = g_twiddle[j];
-  return INV ? conj(w) : w;
+// e^{-2 pi i k / L}
+template <int L>
+__device__ __forceinline__ c32 tw_w(int k) {
+  return g_twiddle[(L - 2) + k];
 }
 
 // --------------------------------------------------------------- codelets
-// In-place DFT of u[0..R-1]; output X[k] in u[k].
+// In-place DFT of u[0..R-1]; output X[k] in u[k].  ZIN: u[R/2..R-1] == 0 on
+// entry (not read).  HOUT: only X[0..R/2-1] are produced.
 
-template <bool INV>
-__device__ __forceinline__ void dft2(c32& a, c32& b) {
-  c32 s = cadd(a, b), d = csub(a, b);
-  a = s; b = d;
-}
-
-template <bool INV>
+template <bool INV, bool ZIN = false, bool HOUT = false>
 __device__ __forceinline__ void dft4(c32& u0, c32& u1, c32& u2, c32& u3) {
-  c32 t0 = cadd(u0, u2), t1 = csub(u0, u2);
-  c32 t2 = cadd(u1, u3), t3 = rot_q<INV>(csub(u1, u3));
-  u0 = cadd(t0, t2); u2 = csub(t0, t2);
-  u1 = cadd(t1, t3); u3 = csub(t1, t3);
+  c32 t0, t1, t2, t3;
+  if constexpr (ZIN) {
+    t0 = u0; t1 = u0; t2 = u1; t3 = rot_q<INV>(u1);
+  } else {
+    t0 = cadd(u0, u2); t1 = csub(u0, u2);
+    t2 = cadd(u1, u3); t3 = rot_q<INV>(csub(u1, u3));
+  }
+  u0 = cadd(t0, t2);
+  u1 = cadd(t1, t3);
+  if constexpr (!HOUT) {
+    u2 = csub(t0, t2);
+    u3 = csub(t1, t3);
+  }
 }
 
-// e^{-+ i pi/4} and e^{-+ 3 i pi/4}
-template <bool INV>
-__device__ __forceinline__ c32 w8_1(c32 a) {
-  const float h = 0.70710678118654752440f;
-  return INV ? scale(mk(a.x - a.y, a.y + a.x), h) : scale(mk(a.x + a.y, a.y - a.x), h);
-}
-template <bool INV>
-__device__ __forceinline__ c32 w8_3(c32 a) {
-  const float h = 0.70710678118654752440f;
-  return INV ? scale(mk(-a.x - a.y, a.x - a.y), h) : scale(mk(a.y - a.x, -a.x - a.y), h);
-}
+constexpr float kH = 0.70710678118654752440f;  // 1/sqrt 2
 
 template <bool INV>
+__device__ __forceinline__ c32 w8_1(c32 a) { return rot_e<INV>(a, kH); }  // e^{-+i pi/4}
+template <bool INV>
+__device__ __forceinline__ c32 w8_3(c32 a) {                           // e^{-+3i pi/4}
+  const c32 p = pmul(a, mk(-kH, -kH));
+  return INV ? pfma(mk(a.y, a.x), mk(-kH, kH), p) : pfma(mk(a.y, a.x), mk(kH, -kH), p);
+}
+
+template <bool INV, bool ZIN = false, bool HOUT = false>
 __device__ __forceinline__ void dft8(c32 (&u)[8]) {
   c32 a[4], b[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    a[k] = cadd(u[k], u[k + 4]);
-    b[k] = csub(u[k], u[k + 4]);
+    if constexpr (ZIN) {
+      a[k] = u[k]; b[k] = u[k];
+    } else {
+      a[k] = cadd(u[k], u[k + 4]); b[k] = csub(u[k], u[k + 4]);
+    }
   }
   b[1] = w8_1<INV>(b[1]);
   b[2] = rot_q<INV>(b[2]);
   b[3] = w8_3<INV>(b[3]);
-  dft4<INV>(a[0], a[1], a[2], a[3]);
-  dft4<INV>(b[0], b[1], b[2], b[3]);
+  dft4<INV, false, HOUT>(a[0], a[1], a[2], a[3]);
+  dft4<INV, false, HOUT>(b[0], b[1], b[2], b[3]);
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < (HOUT ? 2 : 4); ++m) {
     u[2 * m] = a[m];
     u[2 * m + 1] = b[m];
   }
 }
 
 template <bool INV>
-__device__ __forceinline__ c32 w16(c32 a, int e) {  // a * W16^e, e in [0,16)
-  // cos/sin(2 pi e/16)
+__device__ __forceinline__ c32 w16(c32 a, int e) {  // a * W16^e for e in {1,2,3,4,6,9}
   const float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;
-  const float h = 0.70710678118654752440f;
-  switch (e & 15) {
-    case 0: return a;
+  switch (e) {
     case 1: return INV ? cmul(a, mk(c1, s1)) : cmul(a, mk(c1, -s1));
     case 2: return w8_1<INV>(a);
     case 3: return INV ? cmul(a, mk(s1, c1)) : cmul(a, mk(s1, -c1));
     case 4: return rot_q<INV>(a);
     case 6: return w8_3<INV>(a);
-    case 9: return INV ? cmul(a, mk(-c1, -s1)) : cmul(a, mk(-c1, s1));
-    default: {
-      float c = cospif(e / 8.0f), s = sinpif(e / 8.0f);
-      return INV ? cmul(a, mk(c, s)) : cmul(a, mk(c, -s));
-    }
+    default: return INV ? cmul(a, mk(-c1, -s1)) : cmul(a, mk(-c1, s1));  // 9
   }
-  (void)h;
 }
 
-template <bool INV>
+template <bool INV, bool ZIN = false, bool HOUT = false>
 __device__ __forceinline__ void dft16(c32 (&u)[16]) {
+  // 16 = 4 x 4: DFT4 over l of u[k + 4l], twiddle W16^{km}, DFT4 over k -> X[m + 4j]
   c32 y[4][4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    c32 a0 = u[k], a1 = u[k + 4], a2 = u[k + 8], a3 = u[k + 12];
-    dft4<INV>(a0, a1, a2, a3);
+    c32 a0 = u[k], a1 = u[k + 4], a2, a3;
+    if constexpr (!ZIN) { a2 = u[k + 8]; a3 = u[k + 12]; }
+    dft4<INV, ZIN>(a0, a1, a2, a3);
     y[k][0] = a0; y[k][1] = a1; y[k][2] = a2; y[k][3] = a3;
   }
 #pragma unroll
@@ -124,23 +130,29 @@ __device__ __forceinline__ void dft16(c32 (&u)[16]) {
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
     c32 a0 = y[0][m], a1 = y[1][m], a2 = y[2][m], a3 = y[3][m];
-    dft4<INV>(a0, a1, a2, a3);
-    u[m] = a0; u[m + 4] = a1; u[m + 8] = a2; u[m + 12] = a3;
+    dft4<INV, false, HOUT>(a0, a1, a2, a3);
+    u[m] = a0; u[m + 4] = a1;
+    if constexpr (!HOUT) { u[m + 8] = a2; u[m + 12] = a3; }
   }
 }
 
-template <int R, bool INV>
+template <int R, bool INV, bool ZIN, bool HOUT>
 __device__ __forceinline__ void dft(c32 (&u)[R]) {
   if constexpr (R == 1) {
   } else if constexpr (R == 2) {
-    dft2<INV>(u[0], u[1]);
+    if constexpr (ZIN) {
+      u[1] = u[0];
+    } else {
+      const c32 s = cadd(u[0], u[1]), d = csub(u[0], u[1]);
+      u[0] = s; u[1] = d;
+    }
   } else if constexpr (R == 4) {
-    dft4<INV>(u[0], u[1], u[2], u[3]);
+    dft4<INV, ZIN, HOUT>(u[0], u[1], u[2], u[3]);
   } else if constexpr (R == 8) {
-    dft8<INV>(u);
+    dft8<INV, ZIN, HOUT>(u);
   } else {
     static_assert(R == 16, "radix");
-    dft16<INV>(u);
+    dft16<INV, ZIN, HOUT>(u);
   }
 }
 
@@ -150,86 +162,148 @@ template <int M, int E>
 struct FftShape {
   static_assert((M & (M - 1)) == 0 && M >= 2 && M <= TW_MAX, "power-of-two length");
   static_assert(E <= M && (E & (E - 1)) == 0, "E");
-  static constexpr int T = M / E;          // threads per transform
+  static constexpr int T = M / E;  // threads per transform
   static constexpr int L = ilog2(M);
   static constexpr int LE = ilog2(E);
   static constexpr int NP = (L + LE - 1) / LE;  // passes
   static constexpr int LFIRST = L - (NP - 1) * LE;
   __host__ __device__ static constexpr int lradix(int p) { return p == 0 ? LFIRST : LE; }
-  __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : (1 << (LFIRST + (p - 1) * LE)); }
-  static constexpr int SB = group_stride(M);  // smem c32 per group
+  __host__ __device__ static constexpr int ns(int p) {
+    return p == 0 ? 1 : (1 << (LFIRST + (p - 1) * LE));
+  }
 };
 
-template <int M, int E, int P, bool INV>
-__device__ __forceinline__ void fft_pass(c32 (&v)[E], int t) {
+// exchange-buffer word of canonical element m of thread t
+template <int M, int E>
+__device__ __forceinline__ int canon_word(int t, int m) {
+  constexpr int T = M / E;
+  if constexpr (T % 16 == 0) return pad_idx(t) + m * (T + T / 16);
+  else return pad_idx(t + T * m);
+}
+
+// Forward twiddles of pass P for thread t: wp[i][r] = w_i^r, w_i = e^{-2 pi i k_i/(NS R)},
+// k_i = (t + i T) mod NS, from the per-length table and a log-depth product tree.
+template <int M, int E, int P>
+struct PassTw {
+  using S = FftShape<M, E>;
+  static constexpr int R = 1 << S::lradix(P);
+  static constexpr int NS = S::ns(P);
+  static constexpr int ST = E / R;
+  c32 w[ST][R];
+  __device__ __forceinline__ void from_table(int t) {
+#pragma unroll
+    for (int i = 0; i < ST; ++i) {
+      w[i][1] = tw_w<NS * R>((t + i * S::T) & (NS - 1));
+#pragma unroll
+      for (int r = 2; r < R; ++r) w[i][r] = cmul(w[i][r / 2], w[i][r - r / 2]);
+    }
+  }
+};
+
+// default twiddle source: table + product tree
+struct TwTable {
+  template <int M, int E, int P>
+  __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
+    tw.from_table(t);
+  }
+};
+
+template <int M, int E, int P, bool INV, bool ZIN, bool HOUT, int NB>
+__device__ __forceinline__ void fft_pass(c32 (&v)[NB][E], const PassTw<M, E, P>* tw) {
   using S = FftShape<M, E>;
   constexpr int R = 1 << S::lradix(P);
-  constexpr int NS = S::ns(P);
   constexpr int ST = E / R;  // butterflies per thread
 #pragma unroll
   for (int i = 0; i < ST; ++i) {
-    c32 u[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) u[r] = v[i + r * ST];
-    if constexpr (P > 0 && R > 1) {
-      const int b = t + i * S::T;
-      const int k = b & (NS - 1);
-      // w = e^{-2 pi i k / (NS*R)}
-      c32 w = tw_table<INV>(k * (TW_MAX / (NS * R)));
-      c32 wp[R];
-      wp[1] = w;
+    for (int b = 0; b < NB; ++b) {
+      c32 u[R];
 #pragma unroll
-      for (int r = 2; r < R; ++r) wp[r] = cmul(wp[r / 2], wp[r - r / 2]);
+      for (int r = 0; r < (ZIN ? R / 2 : R); ++r) u[r] = v[b][i + r * ST];
+      if constexpr (P > 0 && R > 1) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], wp[r]);
+        for (int r = 1; r < (ZIN ? R / 2 : R); ++r)
+          u[r] = INV ? cmulc(u[r], tw->w[i][r]) : cmul(u[r], tw->w[i][r]);
+      }
+      dft<R, INV, ZIN, HOUT>(u);
+#pragma unroll
+      for (int r = 0; r < (HOUT ? R / 2 : R); ++r) v[b][i + r * ST] = u[r];
     }
-    dft<R, INV>(u);
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[i + r * ST] = u[r];
   }
 }
 
-// write pass-P outputs to the exchange buffer in Stockham order
-template <int M, int E, int P>
-__device__ __forceinline__ void fft_store(const c32 (&v)[E], c32* sm, int t) {
+// write pass-P outputs to the exchange buffer in Stockham order:
+// element (i, r) of butterfly b = t + i T goes to word (b/NS) NS R + b%NS + r NS
+template <int M, int E, int P, int NB>
+__device__ __forceinline__ void fft_store(const c32 (&v)[NB][E], c32* sm, int sbs, int t) {
   using S = FftShape<M, E>;
   constexpr int R = 1 << S::lradix(P);
   constexpr int NS = S::ns(P);
   constexpr int ST = E / R;
 #pragma unroll
   for (int i = 0; i < ST; ++i) {
-    const int b = t + i * S::T;
-    const int base = (b / NS) * NS * R + (b & (NS - 1));
+    const int bf = t + i * S::T;
+    const int base = pad_idx((bf / NS) * NS * R + (bf & (NS - 1)));
+    // base % 16 < NS or NS % 16 == 0, so the padding of base + r NS splits exactly
 #pragma unroll
-    for (int r = 0; r < R; ++r) sm[pad_idx(base + r * NS)] = v[i + r * ST];
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[b * sbs + base + r * NS + ((r * NS) >> 4)] = v[b][i + r * ST];
   }
+}
+
+
+template <int M, int E, int NB>
+__device__ __forceinline__ void load_canonical(c32 (&v)[NB][E], const c32* sm, int sbs, int t) {
+#pragma unroll
+  for (int m = 0; m < E; ++m)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) v[b][m] = sm[b * sbs + canon_word<M, E>(t, m)];
+}
+
+template <int M, int E, int P, bool INV, bool ZIN, bool HOUT, int NB, typename TwF>
+__device__ __forceinline__ void fft_passes_from(c32 (&v)[NB][E], c32* sm, int sbs, int t,
+                                                const TwF& twf) {
+  using S = FftShape<M, E>;
+  constexpr bool LAST = P + 1 == S::NP;
+  if constexpr (P > 0) {
+    PassTw<M, E, P> tw;
+    twf(tw, t);
+    fft_pass<M, E, P, INV, false, HOUT && LAST, NB>(v, &tw);
+  } else {
+    fft_pass<M, E, P, INV, ZIN, HOUT && LAST, NB>(v, (const PassTw<M, E, P>*)nullptr);
+  }
+  if constexpr (!LAST) {
+    fft_store<M, E, P, NB>(v, sm, sbs, t);
+    __syncthreads();
+    load_canonical<M, E, NB>(v, sm, sbs, t);
+    __syncthreads();
+    fft_passes_from<M, E, P + 1, INV, ZIN, HOUT, NB>(v, sm, sbs, t, twf);
+  }
+}
+
+// NB independent transforms per thread (interleaved for ILP, one barrier per
+// exchange): on entry v[b][m] = x_b[t + T m]; on exit v[b][m] = X_b[t + T m].
+// Transform b exchanges through sm + b*sbs.  ZIN: v[b][m] for m >= E/2 is zero
+// (not read).  HOUT: only m < E/2 is valid on exit.  Every thread of the CTA must
+// call it (contains barriers).  twf fills the forward twiddles of passes >= 1.
+template <int M, int E, bool INV, bool ZIN, bool HOUT, int NB, typename TwF = TwTable>
+__device__ __forceinline__ void fftn(c32 (&v)[NB][E], c32* sm, int sbs, int t,
+                                     const TwF& twf = TwF()) {
+  fft_passes_from<M, E, 0, INV, ZIN, HOUT, NB>(v, sm, sbs, t, twf);
+}
+
+// single transform
+template <int M, int E, bool INV, bool ZIN = false, bool HOUT = false>
+__device__ __forceinline__ void fft(c32 (&v)[E], c32* sm, int t) {
+  c32 (&vv)[1][E] = *reinterpret_cast<c32(*)[1][E]>(&v);
+  fftn<M, E, INV, ZIN, HOUT, 1>(vv, sm, 0, t);
 }
 
 template <int M, int E>
-__device__ __forceinline__ void load_canonical(c32 (&v)[E], const c32* sm, int t) {
-  using S = FftShape<M, E>;
+__device__ __forceinline__ void store_canonical(const c32 (&v)[E], c32* sm, int t) {
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = sm[pad_idx(t + S::T * m)];
-}
-
-template <int M, int E, int P, bool INV>
-__device__ __forceinline__ void fft_passes_from(c32 (&v)[E], c32* sm, int t) {
-  using S = FftShape<M, E>;
-  fft_pass<M, E, P, INV>(v, t);
-  if constexpr (P + 1 < S::NP) {
-    fft_store<M, E, P>(v, sm, t);
-    __syncthreads();
-    load_canonical<M, E>(v, sm, t);
-    __syncthreads();
-    fft_passes_from<M, E, P + 1, INV>(v, sm, t);
-  }
-}
-
-// Full transform: on entry v[m] = x[t + T m]; on exit v[m] = X[t + T m].
-// Every thread of the CTA must call it (it contains __syncthreads).
-template <int M, int E, bool INV>
-__device__ __forceinline__ void fft(c32 (&v)[E], c32* sm, int t) {
-  fft_passes_from<M, E, 0, INV>(v, sm, t);
+  for (int m = 0; m < E; ++m) sm[canon_word<M, E>(t, m)] = v[m];
 }
 
 }  // namespace tf

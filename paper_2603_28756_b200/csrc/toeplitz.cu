@@ -7,171 +7,250 @@
 // with the image at offset 0 (exact: all lags |d| <= N-1 stay distinct mod M),
 // and the flip term becomes B = spec(K_flip) * ph(kx) ph(ky),
 // ph_k = e^{-2 pi i k (N-1)/M} (derivation in DESIGN.md §3).  Both lag kernels
-// are real and even, so the transform is real-to-complex on the half spectrum:
+// are real and even, so the transform is real-to-complex on the half spectrum.
 //
-//   K1 k_rows_fwd  : two image rows per complex FFT of length M (zero padded),
-//                    split into two half spectra, stored frequency-major
-//                    T[z][ky][ix] (column ix contiguous for K2).
-//   K2 k_cols_conv : per half-spectrum column ky, length-M FFT over ix,
-//                    Y = F*A + conj(F)*B with the PSF column held in registers
-//                    for the whole slice loop, inverse FFT, keep ix < N.
-//   K3 k_rows_inv  : two rows per complex inverse FFT (Hermitian packing),
-//                    crop n < N, epilogue out = alpha*y + beta*aux.
+// Half-spectrum layout in HBM ("row-blocked"): T[z][rb][ky][r], rb = ix / 4,
+// r = ix % 4, ky in [0, M/2] -- the 4 rows of a block are 32 contiguous bytes
+// per frequency, and one block's whole half spectrum is contiguous.
+//
+//   K1 k_rows_fwd  : each thread runs two complex FFTs (rows 4rb..4rb+3 packed
+//                    pairwise as x_a + i x_b, zero padded to M), splits them
+//                    into four half spectra and writes its block contiguously.
+//   K2 k_cols_conv : per column ky, a TMA 4-D tensor copy gathers the 32-byte
+//                    pieces of all row blocks into shared memory; length-M FFT
+//                    over ix, Y = F*A + conj(F)*B with the PSF column held in
+//                    registers across all slices, inverse FFT, keep ix < N,
+//                    TMA tensor store back in place.
+//   K3 k_rows_inv  : reads a block contiguously, two inverse complex FFTs
+//                    (Hermitian packing), crop n < N, out = alpha*y + beta*aux.
 //
 // PSF (K6, toeplitz.py:85-131 compute_psf/build_psf): the NUFFT-of-ones kernel
 // is replaced by its exact closed form, K(d) = sum_theta D(d . e_theta) with
 // the Dirichlet sum D(u) = sum_j cos(2 pi j u / Nd) over the signed detector
 // frequencies (geometry.py:196-201), K_nyq(d) = 1/2 sum_theta cos(pi d.e_theta)
 // for even Nd (toeplitz.py:106-114); evaluated in fp64, transformed with the
-// same K1 + forward column pass, and folded with 1/M^2 into
+// same K1 + a forward column pass, and folded with 1/M^2 into
 //   PQ = ((A + Re B)/M^2, (A - Re B)/M^2),  Bi = Im B / M^2
 // so that Y = (Fr P + Fi Bi, Fi Q + Fr Bi): two paired-fp32 instructions.
-#include <algorithm>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "tf_async.cuh"
 #include "tf_common.cuh"
 
 namespace tf {
 
+constexpr int RB = 4;  // rows per block of the half-spectrum layout
+__host__ __device__ constexpr int nrb_of(int rows) { return (rows + RB - 1) / RB; }
+
 // ============================================================ K1: rows, forward
-// x: [nslices][rows][row_stride] fp32, row r nonzero for n < n_in (zero beyond)
-// T: [nslices][M/2+1][rows] c32
-template <int M, int E, int F>
-__global__ void __launch_bounds__(F*(M / E))
+// x: [nslices][rows][x_row_stride] fp32, row r nonzero for n < n_in (zero beyond)
+// T: [nslices][nrb][M/2+1][4] c32.  Thread t of group g transforms the block
+// rb = blockIdx.x*G + g as two complex FFTs z_b = x_{4rb+2b} + i x_{4rb+2b+1}
+// and splits them:  X_a(k) = (Z(k) + conj Z(M-k))/2,  X_b(k) = -i (Z(k) - conj Z(M-k))/2.
+// Thread t owns k = t + T m (m < E/2); Z(M-k) sits in the upper half of partner
+// thread T-t and is exchanged through shared memory.  Stores are 32 B per k,
+// contiguous across the warp.  ZP: n_in <= M/2 (upper half of inputs is zero).
+template <int M, int E, int G, bool ZP>
+__global__ void __launch_bounds__(G*(M / E), (M >= 8192 ? 1 : 2))
 k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
            long long x_slice_stride, long long x_row_stride) {
-  using S = FftShape<M, E>;
-  constexpr int TT = S::T;
-  extern __shared__ __align__(16) c32 smem[];
-  const int f = threadIdx.x / TT;
-  const int t = threadIdx.x - f * TT;
-  const int z = blockIdx.y;
-  const int row0 = blockIdx.x * (2 * F);
-  c32* sm = smem + f * S::SB;
-
-  const int ra = row0 + 2 * f, rb = ra + 1;
-  const float* xa = x + z * x_slice_stride + (long long)ra * x_row_stride;
-  const float* xb = xa + x_row_stride;
-  const bool va = ra < rows, vb = rb < rows;
-  c32 v[E];
-#pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const int j = t + TT * m;
-    float a = 0.f, b = 0.f;
-    if (j < n_in) {
-      if (va) a = __ldg(xa + j);
-      if (vb) b = __ldg(xb + j);
-    }
-    v[m] = mk(a, b);
-  }
-  fft<M, E, false>(v, sm, t);
-#pragma unroll
-  for (int m = 0; m < E; ++m) sm[pad_idx(t + TT * m)] = v[m];
-  __syncthreads();
-
-  // X_a(k) = (Z(k) + conj Z(-k))/2 ; X_b(k) = -i (Z(k) - conj Z(-k))/2
+  constexpr int TT = M / E;
+  constexpr int NB = 2;
+  constexpr int SB = group_stride(M, NB * G);
   constexpr int H = M / 2 + 1;
-  c32* Tz = T + (long long)z * H * rows;
-  for (int id = threadIdx.x; id < H * 2 * F; id += blockDim.x) {
-    const int k = id / (2 * F);
-    const int r = id - k * (2 * F);
-    const int row = row0 + r;
-    if (row >= rows) continue;
-    const c32* s = smem + (r >> 1) * S::SB;
-    const c32 zk = s[pad_idx(k)];
-    const c32 zm = s[pad_idx((M - k) & (M - 1))];
-    c32 o;
-    if ((r & 1) == 0)
-      o = scale(mk(zk.x + zm.x, zk.y - zm.y), 0.5f);
-    else
-      o = scale(mk(zk.y + zm.y, zm.x - zk.x), 0.5f);
-    Tz[(long long)k * rows + row] = o;
-  }
-}
-
-// ============================================================ K3: rows, inverse
-// T: [nslices][M/2+1][rows] c32 half spectra; out: [nslices][rows][out_row_stride]
-// out[n] = alpha * y[n] + beta * aux[n]  for n < n_out
-template <int M, int E, int F>
-__global__ void __launch_bounds__(F*(M / E))
-k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __restrict__ aux,
-           int rows, int n_out, long long o_slice_stride, long long o_row_stride, float alpha,
-           float beta) {
-  using S = FftShape<M, E>;
-  constexpr int TT = S::T;
-  constexpr int H = M / 2 + 1;
-  extern __shared__ __align__(16) c32 smem[];
-  const int f = threadIdx.x / TT;
-  const int t = threadIdx.x - f * TT;
-  const int z = blockIdx.y;
-  const int row0 = blockIdx.x * (2 * F);
-  const c32* Tz = T + (long long)z * H * rows;
-
-  // stage the 2F half-spectrum rows: group g holds Ya at [0,H) and Yb at [H,2H)
-  for (int id = threadIdx.x; id < H * 2 * F; id += blockDim.x) {
-    const int k = id / (2 * F);
-    const int r = id - k * (2 * F);
-    const int row = row0 + r;
-    c32 val = mk(0.f, 0.f);
-    if (row < rows) val = Tz[(long long)k * rows + row];
-    if (k == 0 || k == M / 2) val.y = 0.f;  // irfft ignores Im of DC/Nyquist
-    smem[(r >> 1) * S::SB + (r & 1) * H + k] = val;
-  }
-  __syncthreads();
-  c32 v[E];
-  {
-    const c32* s = smem + f * S::SB;
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const int j = t + TT * m;
-      c32 za;
-      if (j <= M / 2) {
-        const c32 ya = s[j], yb = s[H + j];
-        za = mk(ya.x - yb.y, ya.y + yb.x);  // Ya + i Yb
-      } else {
-        const c32 ya = s[M - j], yb = s[H + M - j];
-        za = mk(ya.x + yb.y, yb.x - ya.y);  // conj(Ya) + i conj(Yb)
-      }
-      v[m] = za;
-    }
-  }
-  __syncthreads();
-  fft<M, E, true>(v, smem + f * S::SB, t);
-
-  const int ra = row0 + 2 * f, rb = ra + 1;
-  float* oa = out + z * o_slice_stride + (long long)ra * o_row_stride;
-  float* ob = oa + o_row_stride;
-  const float* aa = aux ? aux + z * o_slice_stride + (long long)ra * o_row_stride : nullptr;
-  const float* ab = aux ? aa + o_row_stride : nullptr;
-#pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const int n = t + TT * m;
-    if (n < n_out) {
-      if (ra < rows) {
-        float y = alpha * v[m].x;
-        if (aa) y = fmaf(beta, __ldg(aa + n), y);
-        oa[n] = y;
-      }
-      if (rb < rows) {
-        float y = alpha * v[m].y;
-        if (ab) y = fmaf(beta, __ldg(ab + n), y);
-        ob[n] = y;
-      }
-    }
-  }
-}
-
-// ============================================================ K2: column convolution
-// T[z][c][0..col_len) in place; PSF columns PQ[c][kx], Bi[c][kx] (kx in [0,M))
-template <int M, int E, int G, bool FLIP>
-__global__ void __launch_bounds__(G*(M / E))
-k_cols_conv(c32* __restrict__ T, const c32* __restrict__ PQ, const float* __restrict__ Bi,
-            int ncols, int col_len, int nslices, long long slice_stride) {
-  using S = FftShape<M, E>;
-  constexpr int TT = S::T;
+  constexpr int EL = ZP ? E / 2 : E;  // loaded elements
   extern __shared__ __align__(16) c32 smem[];
   const int g = threadIdx.x / TT;
   const int t = threadIdx.x - g * TT;
-  c32* sm = smem + g * S::SB;
+  const int z = blockIdx.y;
+  const int nrb = nrb_of(rows);
+  const int rb = blockIdx.x * G + g;
+  const int r0 = rb * RB;
+  c32* sm = smem + g * NB * SB;
+
+  const float* xr = x + z * x_slice_stride + (long long)r0 * x_row_stride;
+  c32 v[NB][E];
+#pragma unroll
+  for (int m = 0; m < EL; ++m) {
+    const int j = t + TT * m;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      float a = 0.f, c = 0.f;
+      if (j < n_in) {
+        if (r0 + 2 * b < rows) a = __ldg(xr + (2 * b) * x_row_stride + j);
+        if (r0 + 2 * b + 1 < rows) c = __ldg(xr + (2 * b + 1) * x_row_stride + j);
+      }
+      v[b][m] = mk(a, c);
+    }
+  }
+  fftn<M, E, false, ZP, false, NB>(v, sm, SB, t);
+  // upper half Z(M/2 + w) -> sm[b][w]; the buffers are free (last pass is register-only)
+#pragma unroll
+  for (int m = E / 2; m < E; ++m)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) sm[b * SB + t + TT * m - M / 2] = v[b][m];
+  __syncthreads();
+  if (rb >= nrb) return;
+
+  float4* dst = reinterpret_cast<float4*>(T + ((long long)z * nrb + rb) * H * RB);
+  auto emit = [&](int k, int m, bool self) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const c32 zk = v[b][m];
+      const c32 zm = self ? zk : sm[b * SB + M / 2 - k];
+      const c32 xa = scale(mk(zk.x + zm.x, zk.y - zm.y), 0.5f);
+      const c32 xb = scale(mk(zk.y + zm.y, zm.x - zk.x), 0.5f);
+      dst[2 * k + b] = make_float4(xa.x, xa.y, xb.x, xb.y);
+    }
+  };
+#pragma unroll
+  for (int m = 0; m < E / 2; ++m) {
+    const int k = t + TT * m;
+    emit(k, m, k == 0);
+  }
+  if (t == 0) emit(M / 2, E / 2, true);
+}
+
+// ============================================================ K3: rows, inverse
+// T: [nslices][nrb][M/2+1][4]; out: [nslices][rows][o_row_stride]
+// out[n] = alpha * y[n] + beta * aux[n] for n < n_out (n_out <= M/2).
+// Thread t of group g inverts block rb's two row pairs with complex FFTs of
+// Z = Y_a + i Y_b (Hermitian extension Z(j) = conj Y_a(M-j) + i conj Y_b(M-j)
+// for j > M/2).  It loads the 32 contiguous bytes of its own k = t + T m
+// (m < E/2); the mirrored half comes from partner thread T-t via shared memory.
+// AUXBULK: the four aux rows are prefetched into shared memory by 1-D bulk
+// copies issued at kernel start (needs 16-byte aligned rows of n_out*4 bytes).
+template <int M, int E, int G, bool AUXBULK>
+__global__ void __launch_bounds__(G*(M / E), (M >= 8192 ? 1 : 2))
+k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __restrict__ aux,
+           int rows, int n_out, long long o_slice_stride, long long o_row_stride, float alpha,
+           float beta) {
+  constexpr int TT = M / E;
+  constexpr int NB = 2;
+  constexpr int H = M / 2 + 1;
+  constexpr int SB = group_stride(M, NB * G);
+  static_assert(2 * H <= SB, "pair buffer must fit the exchange buffer");
+  extern __shared__ __align__(16) c32 smem[];
+  const int g = threadIdx.x / TT;
+  const int t = threadIdx.x - g * TT;
+  const int z = blockIdx.y;
+  const int nrb = nrb_of(rows);
+  const int rb = min(blockIdx.x * G + g, nrb - 1);  // surplus groups redo the last block
+  const bool writer = (int)(blockIdx.x * G + g) < nrb;
+  const int r0 = rb * RB;
+  const float4* src = reinterpret_cast<const float4*>(T + ((long long)z * nrb + rb) * H * RB);
+  c32* sm = smem + g * NB * SB;  // transform b: (Ya, Yb)(k) at words b*SB + 2k, +1
+  // AUXBULK region after the exchange buffers: [G][4][M/2] fp32 + one mbarrier
+  float* auxs = reinterpret_cast<float*>(smem + G * NB * SB) + g * RB * (M / 2);
+  uint64_t* abar = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(smem + G * NB * SB) +
+                                               G * RB * (M / 2));
+  const long long zo = z * o_slice_stride;
+  if constexpr (AUXBULK) {
+    if (threadIdx.x == 0) {
+      mbar_init(abar, G);  // one arrival (with or without tx) per group
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (t == 0 && writer) {
+      const int nr = min(RB, rows - r0);
+      const uint32_t bytes = (uint32_t)n_out * sizeof(float);
+      mbar_expect_tx(abar, nr * bytes);  // one arrival per group
+      for (int q = 0; q < nr; ++q)
+        bulk_g2s(auxs + q * (M / 2), aux + zo + (long long)(r0 + q) * o_row_stride, bytes, abar);
+    } else if (t == 0) {
+      mbar_arrive(abar);
+    }
+  }
+
+  auto fix = [&](int k, float4& y) {
+    if (k == 0 || k == M / 2) { y.y = 0.f; y.w = 0.f; }  // irfft drops Im(DC, Nyquist)
+  };
+  float4 lo[E / 2][NB];
+#pragma unroll
+  for (int m = 0; m < E / 2; ++m)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) lo[m][b] = __ldg(src + 2 * (t + TT * m) + b);
+  float4 nyq[NB];
+  if (t == 0)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) nyq[b] = __ldg(src + 2 * (M / 2) + b);
+#pragma unroll
+  for (int m = 0; m < E / 2; ++m)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      fix(t + TT * m, lo[m][b]);
+      *reinterpret_cast<float4*>(sm + b * SB + 2 * (t + TT * m)) = lo[m][b];
+    }
+  if (t == 0)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      fix(M / 2, nyq[b]);
+      *reinterpret_cast<float4*>(sm + b * SB + 2 * (M / 2)) = nyq[b];
+    }
+  __syncthreads();
+  c32 v[NB][E];
+#pragma unroll
+  for (int m = 0; m < E; ++m)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (m < E / 2) {
+        const float4 y = lo[m][b];
+        v[b][m] = mk(y.x - y.w, y.y + y.z);  // Ya + i Yb
+      } else {
+        const int j = t + TT * m;
+        const float4 y = *reinterpret_cast<const float4*>(sm + b * SB + 2 * (M - j));
+        v[b][m] = mk(y.x + y.w, y.z - y.y);  // conj(Ya) + i conj(Yb)
+      }
+    }
+  __syncthreads();
+  fftn<M, E, true, false, true, NB>(v, sm, SB, t);
+  if constexpr (AUXBULK) mbar_wait(abar, 0);
+  if (!writer) return;
+
+#pragma unroll
+  for (int q = 0; q < RB; ++q) {
+    const int r = r0 + q;
+    if (r >= rows) break;
+    float* o = out + zo + (long long)r * o_row_stride;
+    const float* a = aux ? aux + zo + (long long)r * o_row_stride : nullptr;
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+      const int n = t + TT * m;
+      if (n < n_out) {
+        float y = alpha * ((q & 1) ? v[q >> 1][m].y : v[q >> 1][m].x);
+        if constexpr (AUXBULK) y = fmaf(beta, auxs[q * (M / 2) + n], y);
+        else if (a) y = fmaf(beta, __ldg(a + n), y);
+        o[n] = y;
+      }
+    }
+  }
+}
+
+// element ix of column c of slice z in the row-blocked layout
+__device__ __forceinline__ long long tidx(int z, int ix, int c, int nrb, int H) {
+  return (((long long)z * nrb + (ix >> 2)) * H + c) * RB + (ix & 3);
+}
+
+// ============================================================ K2: column convolution
+// Column c of slice z: elements ix < col_len (zero beyond, col_len <= M/2) of
+// T; PSF columns PQ[c][kx], Bi[c][kx], kx in [0, M).  Generic variant for small
+// M: one column per thread group, slices in sequence, direct gathers.
+template <int M, int E, int G, bool FLIP>
+__global__ void __launch_bounds__(G*(M / E))
+k_cols_conv(c32* __restrict__ T, const c32* __restrict__ PQ, const float* __restrict__ Bi,
+            int ncols, int col_len, int nslices) {
+  constexpr int TT = M / E;
+  constexpr int SB = group_stride(M, G);
+  extern __shared__ __align__(16) c32 smem[];
+  const int g = threadIdx.x / TT;
+  const int t = threadIdx.x - g * TT;
+  const int nrb = nrb_of(col_len);
+  c32* sm = smem + g * SB;
   const int nsteps = (ncols + G * gridDim.x - 1) / (G * gridDim.x);
   for (int step = 0; step < nsteps; ++step) {
     const int c = (step * gridDim.x + blockIdx.x) * G + g;
@@ -181,62 +260,198 @@ k_cols_conv(c32* __restrict__ T, const c32* __restrict__ PQ, const float* __rest
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int kx = t + TT * m;
-      pq[m] = active ? PQ[(long long)c * M + kx] : mk(0.f, 0.f);
-      if constexpr (FLIP) bi[m] = active ? Bi[(long long)c * M + kx] : 0.f;
+      pq[m] = active ? __ldg(PQ + (long long)c * M + kx) : mk(0.f, 0.f);
+      if constexpr (FLIP) bi[m] = active ? __ldg(Bi + (long long)c * M + kx) : 0.f;
     }
-    c32* col = T + (long long)c * col_len;
     for (int z = 0; z < nslices; ++z) {
-      c32* cz = col + z * slice_stride;
       c32 v[E];
 #pragma unroll
-      for (int m = 0; m < E; ++m) {
+      for (int m = 0; m < E / 2; ++m) {
         const int j = t + TT * m;
-        v[m] = (active && j < col_len) ? cz[j] : mk(0.f, 0.f);
+        v[m] = (active && j < col_len) ? T[tidx(z, j, c, nrb, M / 2 + 1)] : mk(0.f, 0.f);
       }
-      fft<M, E, false>(v, sm, t);
+      fft<M, E, false, true, false>(v, sm, t);
 #pragma unroll
       for (int m = 0; m < E; ++m) {
         if constexpr (FLIP) {
           // (Fr P + Fi Bi, Fi Q + Fr Bi)
-          c32 p = pmul(v[m], pq[m]);
-          v[m] = pfma(mk(v[m].y, v[m].x), mk(bi[m], bi[m]), p);
+          v[m] = pfma(mk(v[m].y, v[m].x), mk(bi[m], bi[m]), pmul(v[m], pq[m]));
         } else {
           v[m] = pmul(v[m], pq[m]);
         }
       }
-      // no barrier needed: the forward transform's last shared-memory read is
-      // fenced by the barrier inside fft(), and its last pass is register-only
-      fft<M, E, true>(v, sm, t);
+      // no barrier: the forward transform's last shared-memory read is fenced by
+      // the barrier inside fft(), and its last pass is register-only
+      fft<M, E, true, false, true>(v, sm, t);
 #pragma unroll
-      for (int m = 0; m < E; ++m) {
+      for (int m = 0; m < E / 2; ++m) {
         const int j = t + TT * m;
-        if (active && j < col_len) cz[j] = v[m];
+        if (active && j < col_len) T[tidx(z, j, c, nrb, M / 2 + 1)] = v[m];
       }
     }
   }
 }
 
-// forward-only column FFT (PSF spectra): S[z][c][kx] = FFT_ix(T[z][c][ix])
+// twiddle source for K2: the last pass (k = t for every butterfly) reads a
+// per-thread set precomputed once per kernel; earlier passes use the table
+template <int M, int E>
+struct TwLastCached {
+  using S = FftShape<M, E>;
+  const PassTw<M, E, S::NP - 1>* last;
+  template <int P>
+  __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
+    if constexpr (P == S::NP - 1) tw = *last;
+    else tw.from_table(t);
+  }
+};
+
+// Persistent, TMA-fed K2 for large M.  Each CTA walks its (column, slice-pair)
+// items: NB = 2 slices of one column share the PSF column in registers (and the
+// cached last-pass twiddles).  One thread keeps the next S items in flight:
+// TMA 4-D tensor copies (box = 32 B x BOXR row blocks) gather the column's
+// pieces from every row block into a contiguous shared buffer, completing on
+// the stage's `full` mbarrier.  A stage is refilled only after every thread has
+// arrived on its `empty` mbarrier (release/acquire ordering of the generic
+// reads before the async-proxy write; a bare __syncthreads is not enough since
+// BAR.SYNC lets the issuing warp run ahead).  Results are staged in shared
+// memory and written back in place by TMA tensor stores.
+template <int M, int E, int S, bool FLIP, int NB, bool CACHE>
+__global__ void __launch_bounds__(M / E, (NB == 1 && !CACHE) ? 2 : 1)
+k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ PQ,
+                const float* __restrict__ Bi, int ncols, int nrb, int nslices, int boxr) {
+  constexpr int TT = M / E;
+  constexpr int SB = group_stride(M, NB);
+  constexpr int CL = M / 2;  // column buffer words (>= nrb * 4)
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // [out: NB*CL][stages: S*NB*CL][xbuf: NB*SB][full: S][empty: S]
+  c32* outb = reinterpret_cast<c32*>(smem_raw);
+  c32* inb = outb + NB * CL;
+  c32* xbuf = inb + S * NB * CL;
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + NB * SB);
+  uint64_t* empty = full + S;
+  const int t = threadIdx.x;
+  if ((int)blockIdx.x >= ncols) return;
+  const int my_cols = (ncols - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int pairs = (nslices + NB - 1) / NB;  // items per column
+  const long long nitems = (long long)my_cols * pairs;
+  const int nbox = (nrb + boxr - 1) / boxr;
+  const uint32_t box_bytes = (uint32_t)boxr * RB * sizeof(c32);
+  auto column_of = [&](long long i) { return (int)blockIdx.x + (int)(i / pairs) * (int)gridDim.x; };
+  auto slice_of = [&](long long i, int b) { return NB * (int)(i % pairs) + b; };
+  auto issue = [&](long long i, int s) {
+    const int nb = min(NB, nslices - slice_of(i, 0));
+    mbar_expect_tx(&full[s], nb * nbox * box_bytes);
+    for (int b = 0; b < nb; ++b)
+      for (int q = 0; q < nbox; ++q)
+        tma_load_4d(inb + (s * NB + b) * CL + q * boxr * RB, &tmap, 0, column_of(i), q * boxr,
+                    slice_of(i, b), &full[s]);
+  };
+  if (t == 0) {
+    tma_prefetch_desc(&tmap);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TT);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int s = 0; s < S && s < nitems; ++s) issue(s, s);
+
+  PassTw<M, E, FftShape<M, E>::NP - 1> last_tw;
+  if constexpr (CACHE) last_tw.from_table(t);
+  const TwLastCached<M, E> twc{&last_tw};
+  const TwTable twt;
+  c32 pq[E];
+  float bi[FLIP ? E : 1];
+  const int col_len = nrb * RB;
+  for (long long i = 0; i < nitems; ++i) {
+    const int s = (int)(i % S);
+    const uint32_t parity = (uint32_t)((i / S) & 1);
+    if (i % pairs == 0) {
+      const long long c = column_of(i);
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        pq[m] = __ldg(PQ + c * M + t + TT * m);
+        if constexpr (FLIP) bi[m] = __ldg(Bi + c * M + t + TT * m);
+      }
+    }
+    const int nb = min(NB, nslices - slice_of(i, 0));
+    mbar_wait(&full[s], parity);
+    c32 v[NB][E];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const c32* in = inb + (s * NB + b) * CL;
+#pragma unroll
+      for (int m = 0; m < E / 2; ++m) {
+        const int j = t + TT * m;
+        v[b][m] = (b < nb && j < col_len) ? in[j] : mk(0.f, 0.f);
+      }
+    }
+    mbar_arrive(&empty[s]);
+    if constexpr (CACHE) fftn<M, E, false, true, false, NB>(v, xbuf, SB, t, twc);
+    else fftn<M, E, false, true, false, NB>(v, xbuf, SB, t, twt);
+    // refill stage s with item i + S once every thread has released it
+    if (t == 0 && i + S < nitems) {
+      mbar_wait(&empty[s], parity);
+      issue(i + S, s);
+    }
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if constexpr (FLIP) {
+          v[b][m] = pfma(mk(v[b][m].y, v[b][m].x), mk(bi[m], bi[m]), pmul(v[b][m], pq[m]));
+        } else {
+          v[b][m] = pmul(v[b][m], pq[m]);
+        }
+      }
+    if constexpr (CACHE) fftn<M, E, true, false, true, NB>(v, xbuf, SB, t, twc);
+    else fftn<M, E, true, false, true, NB>(v, xbuf, SB, t, twt);
+    // the previous item's TMA store must have finished reading the out buffer
+    if (t == 0) bulk_wait_read<0>();
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int m = 0; m < E / 2; ++m) {
+        const int j = t + TT * m;
+        if (j < col_len) outb[b * CL + j] = v[b][m];
+      }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (t == 0) {
+      for (int b = 0; b < nb; ++b)
+        for (int q = 0; q < nbox; ++q)
+          tma_store_4d(&tmap, 0, column_of(i), q * boxr, slice_of(i, b),
+                       outb + b * CL + q * boxr * RB);
+      bulk_commit();
+    }
+  }
+  if (t == 0) bulk_wait<0>();
+}
+
+// forward-only column FFT (PSF spectra): S[z][c][kx] = FFT_ix(column c of T)
 template <int M, int E, int G>
 __global__ void __launch_bounds__(G*(M / E))
 k_cols_fwd(const c32* __restrict__ T, c32* __restrict__ Sout, int ncols, int col_len,
-           long long t_slice_stride, long long s_slice_stride) {
-  using S = FftShape<M, E>;
-  constexpr int TT = S::T;
+           long long s_slice_stride) {
+  constexpr int TT = M / E;
   extern __shared__ __align__(16) c32 smem[];
   const int g = threadIdx.x / TT;
   const int t = threadIdx.x - g * TT;
   const int z = blockIdx.y;
   const int c = blockIdx.x * G + g;
   const bool active = c < ncols;
-  const c32* col = T + z * t_slice_stride + (long long)c * col_len;
+  const int nrb = nrb_of(col_len);
   c32 v[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int j = t + TT * m;
-    v[m] = (active && j < col_len) ? col[j] : mk(0.f, 0.f);
+    v[m] = (active && j < col_len) ? T[tidx(z, j, c, nrb, M / 2 + 1)] : mk(0.f, 0.f);
   }
-  fft<M, E, false>(v, smem + g * S::SB, t);
+  fft<M, E, false>(v, smem + g * group_stride(M, G), t);
   if (active) {
     c32* o = Sout + z * s_slice_stride + (long long)c * M;
 #pragma unroll
@@ -305,12 +520,16 @@ __global__ void k_psf_finish(const c32* __restrict__ spec, c32* __restrict__ PQ,
   Bi[id] = (float)bim;
 }
 
+// per-length tables W_L^j at word (L - 2) + j (tf_fft.cuh), computed in fp64
 __global__ void k_twiddle_init(c32* tw) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= TW_MAX) return;
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= TW_WORDS) return;
+  int L = 2;
+  while (w >= 2 * L - 2) L <<= 1;  // table L occupies words [L-2, 2L-2)
+  const int j = w - (L - 2);
   double s, c;
-  sincospi(-2.0 * (double)j / TW_MAX, &s, &c);
-  tw[j] = mk((float)c, (float)s);
+  sincospi(-2.0 * (double)j / L, &s, &c);
+  tw[w] = mk((float)c, (float)s);
 }
 
 
@@ -323,13 +542,13 @@ template <int M>
 constexpr int eper() { return M < E_DEFAULT ? M : E_DEFAULT; }
 
 template <int M>
-constexpr int rows_f() {  // FFTs (row pairs) per CTA in K1/K3
+constexpr int rows_g() {  // thread groups per CTA in K1/K3 (each group: one 4-row block)
   constexpr int T = M / eper<M>();
-  constexpr int f = 512 / T;
-  return f < 1 ? 1 : (f > 16 ? 16 : f);
+  constexpr int g = 256 / T;
+  return g < 1 ? 1 : (g > 16 ? 16 : g);
 }
 template <int M>
-constexpr int cols_g() {  // columns per CTA in K2
+constexpr int cols_g() {  // columns per CTA in the generic K2
   constexpr int T = M / eper<M>();
   constexpr int g = 128 / T;
   return g < 1 ? 1 : g;
@@ -348,18 +567,18 @@ int prep_kernel(K kern, size_t smem) {
 template <int M>
 int launch_rows_fwd(const float* x, c32* T, int rows, int n_in, long long xs, long long xr,
                     long long nslices, cudaStream_t st) {
-  constexpr int E = eper<M>(), F = rows_f<M>();
+  constexpr int E = eper<M>(), G = rows_g<M>();
   constexpr int TT = M / E;
-  const size_t smem = sizeof(c32) * F * FftShape<M, E>::SB;
-  auto kern = k_rows_fwd<M, E, F>;
-  TF_TRY(prep_kernel(kern, smem));
-  const int gx = (rows + 2 * F - 1) / (2 * F);
+  const size_t smem = sizeof(c32) * 2 * G * group_stride(M, 2 * G);
+  const int gx = (nrb_of(rows) + G - 1) / G;
   KernelTimer tm;
   timer_begin(tm, 0, st);
   for (long long z0 = 0; z0 < nslices; z0 += 65535) {
     const int nz = (int)std::min<long long>(65535, nslices - z0);
-    kern<<<dim3(gx, nz), F * TT, smem, st>>>(x + z0 * xs, T + z0 * (long long)(M / 2 + 1) * rows,
-                                             rows, n_in, xs, xr);
+    c32* Tz = T + z0 * (long long)(M / 2 + 1) * RB * nrb_of(rows);
+    auto kern = (2 * n_in <= M) ? k_rows_fwd<M, E, G, true> : k_rows_fwd<M, E, G, false>;
+    TF_TRY(prep_kernel(kern, smem));
+    kern<<<dim3(gx, nz), G * TT, smem, st>>>(x + z0 * xs, Tz, rows, n_in, xs, xr);
   }
   timer_end(tm);
   return check_launch("k_rows_fwd");
@@ -369,54 +588,129 @@ template <int M>
 int launch_rows_inv(const c32* T, float* out, const float* aux, int rows, int n_out,
                     long long os, long long orow, float alpha, float beta, long long nslices,
                     cudaStream_t st) {
-  constexpr int E = eper<M>(), F = rows_f<M>();
+  constexpr int E = eper<M>(), G = rows_g<M>();
   constexpr int TT = M / E;
-  const size_t smem = sizeof(c32) * F * FftShape<M, E>::SB;
-  auto kern = k_rows_inv<M, E, F>;
+  if (2 * n_out > M) return fail_arg("k_rows_inv: n_out %d exceeds M/2", n_out);
+  // bulk-prefetch aux rows when they are 16-byte aligned blocks
+  const bool bulk = aux && (n_out % 4 == 0) && (orow % 4 == 0) && (os % 4 == 0) &&
+                    (reinterpret_cast<uintptr_t>(aux) % 16 == 0);
+  const size_t smem = sizeof(c32) * 2 * G * group_stride(M, 2 * G) +
+                      (bulk ? sizeof(float) * G * RB * (M / 2) + 16 : 0);
+  auto kern = bulk ? k_rows_inv<M, E, G, true> : k_rows_inv<M, E, G, false>;
   TF_TRY(prep_kernel(kern, smem));
-  const int gx = (rows + 2 * F - 1) / (2 * F);
+  const int gx = (nrb_of(rows) + G - 1) / G;
   KernelTimer tm;
   timer_begin(tm, 2, st);
   for (long long z0 = 0; z0 < nslices; z0 += 65535) {
     const int nz = (int)std::min<long long>(65535, nslices - z0);
-    kern<<<dim3(gx, nz), F * TT, smem, st>>>(T + z0 * (long long)(M / 2 + 1) * rows, out + z0 * os,
-                                             aux ? aux + z0 * os : nullptr, rows, n_out, os, orow,
-                                             alpha, beta);
+    kern<<<dim3(gx, nz), G * TT, smem, st>>>(T + z0 * (long long)(M / 2 + 1) * RB * nrb_of(rows),
+                                             out + z0 * os, aux ? aux + z0 * os : nullptr, rows,
+                                             n_out, os, orow, alpha, beta);
   }
   timer_end(tm);
   return check_launch("k_rows_inv");
 }
 
-template <int M>
-int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
-                     bool flip, cudaStream_t st) {
+// 4-D tensor map over the row-blocked half spectrum: dims (fp32 units)
+// {8 = 4 rows x re/im, M/2+1 columns, nrb row blocks, nslices}; box {8, 1, boxr, 1}
+int encode_tmap(CUtensorMap* map, c32* T, int M, int nrb, long long nslices, int boxr) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    TF_TRY(check_cuda(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+                      "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)"));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return TF_ECUDA;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t H = M / 2 + 1;
+  const cuuint64_t dims[4] = {8, H, (cuuint64_t)nrb, (cuuint64_t)nslices};
+  const cuuint64_t strides[3] = {32, H * 32, H * 32 * (cuuint64_t)nrb};
+  const cuuint32_t box[4] = {8, 1, (cuuint32_t)boxr, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return TF_ECUDA;
+  }
+  return TF_OK;
+}
+
+constexpr int CONV_STAGES = 2;
+
+template <int M, bool FLIP, int NB, bool CACHE>
+int launch_cols_conv_tma_t(c32* T, const c32* PQ, const float* Bi, int col_len,
+                           long long nslices, cudaStream_t st) {
+  constexpr int E = eper<M>();
+  constexpr int TT = M / E;
+  const int ncols = M / 2 + 1;
+  const int nrb = nrb_of(col_len);
+  const int boxr = std::min(nrb, 256);
+  CUtensorMap map;
+  TF_TRY(encode_tmap(&map, T, M, nrb, nslices, boxr));
+  const size_t smem = sizeof(c32) * ((size_t)(1 + CONV_STAGES) * NB * (M / 2) + NB * group_stride(M, NB)) +
+                      2 * CONV_STAGES * sizeof(uint64_t);
+  auto kern = k_cols_conv_tma<M, E, CONV_STAGES, FLIP, NB, CACHE>;
+  TF_TRY(prep_kernel(kern, smem));
+  int blocks_per_sm = 0;
+  TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, TT, smem),
+                    "occupancy"));
+  const int grid = std::max(1, std::min(ncols, std::max(1, blocks_per_sm) * num_sms()));
+  KernelTimer tm;
+  timer_begin(tm, 1, st);
+  kern<<<grid, TT, smem, st>>>(map, PQ, Bi, ncols, nrb, (int)nslices, boxr);
+  timer_end(tm);
+  return check_launch("k_cols_conv_tma");
+}
+
+template <int M, bool FLIP>
+int launch_cols_conv_t(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
+                       cudaStream_t st) {
   constexpr int E = eper<M>(), G = cols_g<M>();
   constexpr int TT = M / E;
   const int ncols = M / 2 + 1;
-  const size_t smem = sizeof(c32) * G * FftShape<M, E>::SB;
+  const size_t smem = sizeof(c32) * G * group_stride(M, G);
+  auto kern = k_cols_conv<M, E, G, FLIP>;
+  TF_TRY(prep_kernel(kern, smem));
   int blocks_per_sm = 0;
-  int grid = 0;
-  const long long sstride = (long long)(M / 2 + 1) * col_len;
+  TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, G * TT, smem),
+                    "occupancy"));
+  const int grid = std::max(1, std::min((ncols + G - 1) / G, blocks_per_sm * num_sms()));
   KernelTimer tm;
-  if (flip) {
-    auto kern = k_cols_conv<M, E, G, true>;
-    TF_TRY(prep_kernel(kern, smem));
-    TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, G * TT, smem),
-                      "occupancy"));
-    grid = std::max(1, std::min((ncols + G - 1) / G, blocks_per_sm * num_sms()));
-    timer_begin(tm, 1, st);
-    kern<<<grid, G * TT, smem, st>>>(T, PQ, Bi, ncols, col_len, (int)nslices, sstride);
-  } else {
-    auto kern = k_cols_conv<M, E, G, false>;
-    TF_TRY(prep_kernel(kern, smem));
-    TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, G * TT, smem),
-                      "occupancy"));
-    grid = std::max(1, std::min((ncols + G - 1) / G, blocks_per_sm * num_sms()));
-    timer_begin(tm, 1, st);
-    kern<<<grid, G * TT, smem, st>>>(T, PQ, Bi, ncols, col_len, (int)nslices, sstride);
-  }
+  timer_begin(tm, 1, st);
+  kern<<<grid, G * TT, smem, st>>>(T, PQ, Bi, ncols, col_len, (int)nslices);
   timer_end(tm);
   return check_launch("k_cols_conv");
+}
+
+template <int M>
+int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
+                     bool flip, cudaStream_t st) {
+  if (2 * col_len > M) return fail_arg("k_cols_conv: column length %d exceeds M/2", col_len);
+  // tuning/debug knob: TF_K2 = generic | nb1 | nb1c | nb2 | nb2c (default nb1)
+  static const char* k2 = getenv("TF_K2");
+  static const int variant = !k2 ? 0 : !strcmp(k2, "generic") ? -1 : !strcmp(k2, "nb1") ? 0
+                          : !strcmp(k2, "nb1c") ? 1 : !strcmp(k2, "nb2") ? 2 : 3;
+  if constexpr (M >= 1024 && M <= 4096) {
+    switch (variant) {
+      case 0: return flip ? launch_cols_conv_tma_t<M, true, 1, false>(T, PQ, Bi, col_len, nslices, st)
+                          : launch_cols_conv_tma_t<M, false, 1, false>(T, PQ, Bi, col_len, nslices, st);
+      case 1: return flip ? launch_cols_conv_tma_t<M, true, 1, true>(T, PQ, Bi, col_len, nslices, st)
+                          : launch_cols_conv_tma_t<M, false, 1, true>(T, PQ, Bi, col_len, nslices, st);
+      case 2: return flip ? launch_cols_conv_tma_t<M, true, 2, false>(T, PQ, Bi, col_len, nslices, st)
+                          : launch_cols_conv_tma_t<M, false, 2, false>(T, PQ, Bi, col_len, nslices, st);
+      case 3: return flip ? launch_cols_conv_tma_t<M, true, 2, true>(T, PQ, Bi, col_len, nslices, st)
+                          : launch_cols_conv_tma_t<M, false, 2, true>(T, PQ, Bi, col_len, nslices, st);
+      default: break;
+    }
+  }
+  return flip ? launch_cols_conv_t<M, true>(T, PQ, Bi, col_len, nslices, st)
+              : launch_cols_conv_t<M, false>(T, PQ, Bi, col_len, nslices, st);
 }
 
 template <int M>
@@ -424,11 +718,11 @@ int launch_cols_fwd(const c32* T, c32* Sout, int col_len, long long nslices, cud
   constexpr int E = eper<M>(), G = cols_g<M>();
   constexpr int TT = M / E;
   const int ncols = M / 2 + 1;
-  const size_t smem = sizeof(c32) * G * FftShape<M, E>::SB;
+  const size_t smem = sizeof(c32) * G * group_stride(M, G);
   auto kern = k_cols_fwd<M, E, G>;
   TF_TRY(prep_kernel(kern, smem));
   kern<<<dim3((ncols + G - 1) / G, (unsigned)nslices), G * TT, smem, st>>>(
-      T, Sout, ncols, col_len, (long long)ncols * col_len, (long long)ncols * M);
+      T, Sout, ncols, col_len, (long long)ncols * M);
   return check_launch("k_cols_fwd");
 }
 
@@ -472,7 +766,7 @@ template <int M>
 struct PsfFn {
   static int run(int n, const double* cs, int n_angles, int nd, c32* PQ, float* Bi, char* ws,
                  cudaStream_t st) {
-    // ws: lags [2][M][M] f32 | T [2][M/2+1][M] c32 | spec [2][M/2+1][M] c32
+    // ws: lags [2][M][M] f32 | T [2][M/4][M/2+1][4] c32 | spec [2][M/2+1][M] c32
     const long long MM = (long long)M * M;
     const long long H = M / 2 + 1;
     float* lags = reinterpret_cast<float*>(ws);
@@ -502,7 +796,7 @@ struct PsfFn {
 int toeplitz_apply(const float* x, float* out, const float* aux, float alpha, float beta,
                    long long nslices, int n, int M, const void* PQ, const float* Bi, bool flip,
                    void* ws, size_t ws_bytes, cudaStream_t st) {
-  const long long per = (long long)(M / 2 + 1) * n * (long long)sizeof(c32);
+  const long long per = (long long)(M / 2 + 1) * RB * nrb_of(n) * (long long)sizeof(c32);
   const long long chunk = (long long)(ws_bytes / per);
   if (chunk < 1) return fail_arg("toeplitz workspace too small: %zu < %lld", ws_bytes, per);
   return dispatch_m<ApplyFn>(M, x, out, aux, alpha, beta, nslices, n,
@@ -525,7 +819,7 @@ int psf_build(int n, int M, const double* cs, int n_angles, int nd, void* PQ, fl
 int init_twiddles() {
   c32* p = nullptr;
   TF_TRY(check_cuda(cudaGetSymbolAddress((void**)&p, g_twiddle), "cudaGetSymbolAddress"));
-  k_twiddle_init<<<(TW_MAX + 255) / 256, 256>>>(p);
+  k_twiddle_init<<<(TW_WORDS + 255) / 256, 256>>>(p);
   TF_TRY(check_launch("k_twiddle_init"));
   return check_cuda(cudaDeviceSynchronize(), "twiddle init sync");
 }
