@@ -66,6 +66,35 @@ long long tf_reduce_workspace_bytes(void);
 int tf_dot2(const float* d_x, const float* d_a, const float* d_b, long long n, double* d_out,
             double* d_ws, void* stream);
 
+/* ---- qGGMRF prior + momentum update (K4) and objective reductions (K5) ----
+ * Volumes [nz][h][w] (w contiguous); *_lo / *_hi are optional halo planes (z = -1, z = nz) of a
+ * slab (NULL: cliques across that face are dropped, qggmrf.py:142-160).
+ * weights3 (HOST pointer): stencil weights for offsets with 1, 2, 3 nonzero
+ * components (3-D: face, edge, corner; 2-D: face, diagonal, unused), as
+ * _build_stencil (qggmrf.py:86-97).  d_ws: tf_prior_workspace_bytes(n). */
+long long tf_prior_workspace_bytes(int h, int w);
+
+/* y = f + c (f - f_prev), K y = K f + c (K f - K f_prev),
+ * grad = K y - R*g + lam * sum_s b_s rho'(y_v - y_{v+s})  (prior_grad, qggmrf.py:172-189);
+ * write_grad = 0: out = y - grad * inv_L (clamped at 0 if nonneg) -- solver.py:149-156;
+ * write_grad = 1: out = grad.  d_Kf/d_Kfp/d_rstar may be NULL (treated as 0).
+ * *d_gsq = sum grad^2 (fp64). */
+int tf_prior_update(const float* d_f, const float* d_f_lo, const float* d_f_hi, const float* d_fp,
+                    const float* d_fp_lo, const float* d_fp_hi, const float* d_Kf,
+                    const float* d_Kfp, const float* d_rstar, float* d_out, int nz, int h, int w,
+                    float c, float lam, float inv_L, int nonneg, int write_grad, int three_d,
+                    double sigma, double p, double q, double T, const double* weights3,
+                    double* d_ws, double* d_gsq, void* stream);
+
+/* d_out3 (fp64) = { E(f_new) over the half stencil plus pairs into d_fn_hi
+ *   (prior_energy, qggmrf.py:192-217; 0 if !with_prior),
+ *   <f_new, K f_new / 2 - R*g>  (fidelity minus g'g/2, toeplitz.py:226-230),
+ *   <f_new - f, (K f_new + K f)/2 - R*g>  (fidelity increment; 0 if d_f NULL) }. */
+int tf_energy_fid(const float* d_fn, const float* d_fn_hi, const float* d_f, const float* d_Kfn,
+                  const float* d_Kf, const float* d_rstar, int nz, int h, int w, int with_prior,
+                  int three_d, double sigma, double p, double q, double T, const double* weights3,
+                  double* d_ws, double* d_out3, void* stream);
+
 /* Per-kernel CUDA-event timing used by bench.py for the roofline numbers.
  * Enable (clears totals), run, then collect: ms_out[slot] = total ms and
  * n_out[slot] = launches per slot (0 k_rows_fwd, 1 k_cols_conv, 2 k_rows_inv). */

@@ -40,6 +40,14 @@ _SIGNATURES = {
     "tf_reduce_workspace_bytes": (_c_ll, []),
     "tf_dot2": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_ll, _c_void_p, _c_void_p,
                          _c_void_p]),
+    "tf_prior_workspace_bytes": (_c_ll, [_c_int, _c_int]),
+    "tf_prior_update": (_c_int, [_c_void_p] * 10 + [_c_int, _c_int, _c_int, _c_float, _c_float, _c_float,
+                                                    _c_int, _c_int, _c_int, _c_double, _c_double,
+                                                    _c_double, _c_double, _c_void_p, _c_void_p,
+                                                    _c_void_p, _c_void_p]),
+    "tf_energy_fid": (_c_int, [_c_void_p] * 6 + [_c_int, _c_int, _c_int, _c_int, _c_int, _c_double,
+                                                 _c_double, _c_double, _c_double, _c_void_p,
+                                                 _c_void_p, _c_void_p, _c_void_p]),
     "tf_timing_enable": (_c_int, [_c_int]),
     "tf_timing_collect": (_c_int, [_c_void_p, _c_void_p, _c_int]),
 }

@@ -100,6 +100,17 @@ size_t psf_workspace_bytes(int M);
 int psf_build(int n, int M, const double* cs, int n_angles, int nd, void* PQ, float* Bi,
               void* ws, size_t ws_bytes, cudaStream_t st);
 int reduce_blocks();
+long long prior_partials(int h, int w);
+int prior_update(const float* f, const float* f_lo, const float* f_hi, const float* fp,
+                 const float* fp_lo, const float* fp_hi, const float* Kf, const float* Kfp,
+                 const float* rstar, float* f_new, int nz, int h, int w_, float c, float lam,
+                 float inv_L, int nonneg, int write_grad, int three_d, double sigma, double p,
+                 double q, double T, const double* w, double* partial, double* out_gsq,
+                 cudaStream_t st);
+int energy_fid(const float* fn, const float* fn_hi, const float* f, const float* Kfn,
+               const float* Kf, const float* rstar, int nz, int h, int w_, int with_prior,
+               int three_d, double sigma, double p, double q, double T, const double* w,
+               double* partial, double* out3, cudaStream_t st);
 int dot2(const float* x, const float* a, const float* b, long long n, double* out, double* ws,
          cudaStream_t st);
 
@@ -165,6 +176,47 @@ int tf_dot2(const float* d_x, const float* d_a, const float* d_b, long long n, d
   TF_TRY(ensure_init());
   if (n < 0 || !d_x || !d_a || !d_out || !d_ws) return fail_arg("bad tf_dot2 arguments");
   return dot2(d_x, d_a, d_b, n, d_out, d_ws, (cudaStream_t)stream);
+}
+
+long long tf_prior_workspace_bytes(int h, int w) {
+  if (h < 1 || w < 1) return fail_arg("bad slice shape");
+  return prior_partials(h, w) * 3 * (long long)sizeof(double);
+}
+
+static int check_prior(int h, int w, int nz, double sigma, double p, double q, double T) {
+  if (h < 1 || w < 1 || nz < 1) return fail_arg("bad volume shape (%d x %d x %d)", nz, h, w);
+  if (!(1.0 <= q && q < p && p <= 2.0)) return fail_arg("require 1 <= q < p <= 2");
+  if (!(sigma > 0) || !(T > 0)) return fail_arg("sigma and T must be positive");
+  return TF_OK;
+}
+
+int tf_prior_update(const float* d_f, const float* d_f_lo, const float* d_f_hi, const float* d_fp,
+                    const float* d_fp_lo, const float* d_fp_hi, const float* d_Kf,
+                    const float* d_Kfp, const float* d_rstar, float* d_out, int nz, int h, int w,
+                    float c, float lam, float inv_L, int nonneg, int write_grad, int three_d,
+                    double sigma, double p, double q, double T, const double* weights3,
+                    double* d_ws, double* d_gsq, void* stream) {
+  TF_TRY(ensure_init());
+  TF_TRY(check_prior(h, w, nz, sigma, p, q, T));
+  if (!d_f || !d_fp || !d_out || !d_ws || !d_gsq || !weights3) return fail_arg("null pointer");
+  if ((d_Kf == nullptr) != (d_Kfp == nullptr)) return fail_arg("Kf and Kfp must both be given");
+  if ((d_f_lo == nullptr) != (d_fp_lo == nullptr) || (d_f_hi == nullptr) != (d_fp_hi == nullptr))
+    return fail_arg("halo planes of f and f_prev must both be given");
+  return prior_update(d_f, d_f_lo, d_f_hi, d_fp, d_fp_lo, d_fp_hi, d_Kf, d_Kfp, d_rstar, d_out, nz,
+                      h, w, c, lam, inv_L, nonneg, write_grad, three_d, sigma, p, q, T, weights3, d_ws,
+                      d_gsq, (cudaStream_t)stream);
+}
+
+int tf_energy_fid(const float* d_fn, const float* d_fn_hi, const float* d_f, const float* d_Kfn,
+                  const float* d_Kf, const float* d_rstar, int nz, int h, int w, int with_prior,
+                  int three_d, double sigma, double p, double q, double T, const double* weights3,
+                  double* d_ws, double* d_out3, void* stream) {
+  TF_TRY(ensure_init());
+  TF_TRY(check_prior(h, w, nz, sigma, p, q, T));
+  if (!d_fn || !d_ws || !d_out3 || !weights3) return fail_arg("null pointer");
+  if (d_f && (!d_Kf || !d_Kfn)) return fail_arg("increment needs Kf and Kf_new");
+  return energy_fid(d_fn, d_fn_hi, d_f, d_Kfn, d_Kf, d_rstar, nz, h, w, with_prior, three_d, sigma, p,
+                    q, T, weights3, d_ws, d_out3, (cudaStream_t)stream);
 }
 
 int tf_timing_enable(int on) {

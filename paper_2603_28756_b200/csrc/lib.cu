@@ -3,3 +3,4 @@
 #include "capi.cu"
 #include "toeplitz.cu"
 #include "reduce.cu"
+#include "qggmrf.cu"

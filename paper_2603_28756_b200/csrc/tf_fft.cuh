@@ -261,7 +261,7 @@ __device__ __forceinline__ void load_canonical(c32 (&v)[NB][E], const c32* sm, i
     for (int b = 0; b < NB; ++b) v[b][m] = sm[b * sbs + canon_word<M, E>(t, m)];
 }
 
-template <int M, int E, int P, bool INV, bool ZIN, bool HOUT, int NB, typename TwF>
+template <int M, int E, int P, bool INV, bool ZIN, bool HOUT, int NB, bool PP, typename TwF>
 __device__ __forceinline__ void fft_passes_from(c32 (&v)[NB][E], c32* sm, int sbs, int t,
                                                 const TwF& twf) {
   using S = FftShape<M, E>;
@@ -274,23 +274,30 @@ __device__ __forceinline__ void fft_passes_from(c32 (&v)[NB][E], c32* sm, int sb
     fft_pass<M, E, P, INV, ZIN, HOUT && LAST, NB>(v, (const PassTw<M, E, P>*)nullptr);
   }
   if constexpr (!LAST) {
-    fft_store<M, E, P, NB>(v, sm, sbs, t);
+    // ping-pong: exchange P uses buffer half P % 2, so the next exchange's stores
+    // cannot overwrite words still being read and the trailing barrier goes away
+    c32* buf = (PP && (P & 1)) ? sm + NB * sbs : sm;
+    fft_store<M, E, P, NB>(v, buf, sbs, t);
     __syncthreads();
-    load_canonical<M, E, NB>(v, sm, sbs, t);
-    __syncthreads();
-    fft_passes_from<M, E, P + 1, INV, ZIN, HOUT, NB>(v, sm, sbs, t, twf);
+    load_canonical<M, E, NB>(v, buf, sbs, t);
+    if constexpr (!PP) __syncthreads();
+    fft_passes_from<M, E, P + 1, INV, ZIN, HOUT, NB, PP>(v, sm, sbs, t, twf);
   }
 }
 
 // NB independent transforms per thread (interleaved for ILP, one barrier per
 // exchange): on entry v[b][m] = x_b[t + T m]; on exit v[b][m] = X_b[t + T m].
-// Transform b exchanges through sm + b*sbs.  ZIN: v[b][m] for m >= E/2 is zero
-// (not read).  HOUT: only m < E/2 is valid on exit.  Every thread of the CTA must
-// call it (contains barriers).  twf fills the forward twiddles of passes >= 1.
-template <int M, int E, bool INV, bool ZIN, bool HOUT, int NB, typename TwF = TwTable>
+// Transform b exchanges through sm + b*sbs (PP: also sm + (NB+b)*sbs, used on
+// odd exchanges; valid back-to-back only when every call makes an even number of
+// exchanges, i.e. NP odd).  ZIN: v[b][m] for m >= E/2 is zero (not read).  HOUT:
+// only m < E/2 is valid on exit.  Every thread of the CTA must call it
+// (contains barriers).  twf fills the forward twiddles of passes >= 1.
+template <int M, int E, bool INV, bool ZIN, bool HOUT, int NB, typename TwF = TwTable,
+          bool PP = false>
 __device__ __forceinline__ void fftn(c32 (&v)[NB][E], c32* sm, int sbs, int t,
                                      const TwF& twf = TwF()) {
-  fft_passes_from<M, E, 0, INV, ZIN, HOUT, NB>(v, sm, sbs, t, twf);
+  static_assert(!PP || (FftShape<M, E>::NP % 2 == 1), "ping-pong needs an even exchange count");
+  fft_passes_from<M, E, 0, INV, ZIN, HOUT, NB, PP>(v, sm, sbs, t, twf);
 }
 
 // single transform

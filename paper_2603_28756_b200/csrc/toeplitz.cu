@@ -315,19 +315,22 @@ struct TwLastCached {
 // reads before the async-proxy write; a bare __syncthreads is not enough since
 // BAR.SYNC lets the issuing warp run ahead).  Results are staged in shared
 // memory and written back in place by TMA tensor stores.
-template <int M, int E, int S, bool FLIP, int NB, bool CACHE>
+// PP: ping-pong exchange buffers (one barrier per exchange) and direct stores
+// of the results (8-byte lanes, 32-byte sector-complete) instead of TMA stores.
+template <int M, int E, int S, bool FLIP, int NB, bool CACHE, bool PP>
 __global__ void __launch_bounds__(M / E, (NB == 1 && !CACHE) ? 2 : 1)
 k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ PQ,
-                const float* __restrict__ Bi, int ncols, int nrb, int nslices, int boxr) {
+                const float* __restrict__ Bi, int ncols, int nrb, int nslices, int boxr,
+                c32* __restrict__ T) {
   constexpr int TT = M / E;
   constexpr int SB = group_stride(M, NB);
   constexpr int CL = M / 2;  // column buffer words (>= nrb * 4)
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // [out: NB*CL][stages: S*NB*CL][xbuf: NB*SB][full: S][empty: S]
+  // [out: NB*CL unless PP][stages: S*NB*CL][xbuf: NB*SB (x2 if PP)][full: S][empty: S]
   c32* outb = reinterpret_cast<c32*>(smem_raw);
-  c32* inb = outb + NB * CL;
+  c32* inb = outb + (PP ? 0 : NB * CL);
   c32* xbuf = inb + S * NB * CL;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + NB * SB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + (PP ? 2 : 1) * NB * SB);
   uint64_t* empty = full + S;
   const int t = threadIdx.x;
   if ((int)blockIdx.x >= ncols) return;
@@ -390,8 +393,8 @@ k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict_
       }
     }
     mbar_arrive(&empty[s]);
-    if constexpr (CACHE) fftn<M, E, false, true, false, NB>(v, xbuf, SB, t, twc);
-    else fftn<M, E, false, true, false, NB>(v, xbuf, SB, t, twt);
+    if constexpr (CACHE) fftn<M, E, false, true, false, NB, TwLastCached<M, E>, PP>(v, xbuf, SB, t, twc);
+    else fftn<M, E, false, true, false, NB, TwTable, PP>(v, xbuf, SB, t, twt);
     // refill stage s with item i + S once every thread has released it
     if (t == 0 && i + S < nitems) {
       mbar_wait(&empty[s], parity);
@@ -407,8 +410,21 @@ k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict_
           v[b][m] = pmul(v[b][m], pq[m]);
         }
       }
-    if constexpr (CACHE) fftn<M, E, true, false, true, NB>(v, xbuf, SB, t, twc);
-    else fftn<M, E, true, false, true, NB>(v, xbuf, SB, t, twt);
+    if constexpr (CACHE) fftn<M, E, true, false, true, NB, TwLastCached<M, E>, PP>(v, xbuf, SB, t, twc);
+    else fftn<M, E, true, false, true, NB, TwTable, PP>(v, xbuf, SB, t, twt);
+    if constexpr (PP) {
+      const int H = M / 2 + 1;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (b >= nb) break;
+#pragma unroll
+        for (int m = 0; m < E / 2; ++m) {
+          const int j = t + TT * m;
+          if (j < col_len) T[tidx(slice_of(i, b), j, column_of(i), nrb, H)] = v[b][m];
+        }
+      }
+      continue;
+    }
     // the previous item's TMA store must have finished reading the out buffer
     if (t == 0) bulk_wait_read<0>();
     __syncthreads();
@@ -643,7 +659,7 @@ int encode_tmap(CUtensorMap* map, c32* T, int M, int nrb, long long nslices, int
 
 constexpr int CONV_STAGES = 2;
 
-template <int M, bool FLIP, int NB, bool CACHE>
+template <int M, bool FLIP, int NB, bool CACHE, bool PP = false>
 int launch_cols_conv_tma_t(c32* T, const c32* PQ, const float* Bi, int col_len,
                            long long nslices, cudaStream_t st) {
   constexpr int E = eper<M>();
@@ -653,9 +669,10 @@ int launch_cols_conv_tma_t(c32* T, const c32* PQ, const float* Bi, int col_len,
   const int boxr = std::min(nrb, 256);
   CUtensorMap map;
   TF_TRY(encode_tmap(&map, T, M, nrb, nslices, boxr));
-  const size_t smem = sizeof(c32) * ((size_t)(1 + CONV_STAGES) * NB * (M / 2) + NB * group_stride(M, NB)) +
+  const size_t smem = sizeof(c32) * ((size_t)((PP ? 0 : 1) + CONV_STAGES) * NB * (M / 2) +
+                                     (PP ? 2 : 1) * NB * group_stride(M, NB)) +
                       2 * CONV_STAGES * sizeof(uint64_t);
-  auto kern = k_cols_conv_tma<M, E, CONV_STAGES, FLIP, NB, CACHE>;
+  auto kern = k_cols_conv_tma<M, E, CONV_STAGES, FLIP, NB, CACHE, PP>;
   TF_TRY(prep_kernel(kern, smem));
   int blocks_per_sm = 0;
   TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, TT, smem),
@@ -663,7 +680,7 @@ int launch_cols_conv_tma_t(c32* T, const c32* PQ, const float* Bi, int col_len,
   const int grid = std::max(1, std::min(ncols, std::max(1, blocks_per_sm) * num_sms()));
   KernelTimer tm;
   timer_begin(tm, 1, st);
-  kern<<<grid, TT, smem, st>>>(map, PQ, Bi, ncols, nrb, (int)nslices, boxr);
+  kern<<<grid, TT, smem, st>>>(map, PQ, Bi, ncols, nrb, (int)nslices, boxr, T);
   timer_end(tm);
   return check_launch("k_cols_conv_tma");
 }
@@ -695,7 +712,7 @@ int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long l
   // tuning/debug knob: TF_K2 = generic | nb1 | nb1c | nb2 | nb2c (default nb1)
   static const char* k2 = getenv("TF_K2");
   static const int variant = !k2 ? 0 : !strcmp(k2, "generic") ? -1 : !strcmp(k2, "nb1") ? 0
-                          : !strcmp(k2, "nb1c") ? 1 : !strcmp(k2, "nb2") ? 2 : 3;
+                          : !strcmp(k2, "nb1c") ? 1 : !strcmp(k2, "nb2") ? 2 : !strcmp(k2, "nb1p") ? 4 : 3;
   if constexpr (M >= 1024 && M <= 4096) {
     switch (variant) {
       case 0: return flip ? launch_cols_conv_tma_t<M, true, 1, false>(T, PQ, Bi, col_len, nslices, st)
@@ -706,6 +723,8 @@ int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long l
                           : launch_cols_conv_tma_t<M, false, 2, false>(T, PQ, Bi, col_len, nslices, st);
       case 3: return flip ? launch_cols_conv_tma_t<M, true, 2, true>(T, PQ, Bi, col_len, nslices, st)
                           : launch_cols_conv_tma_t<M, false, 2, true>(T, PQ, Bi, col_len, nslices, st);
+      case 4: return flip ? launch_cols_conv_tma_t<M, true, 1, false, true>(T, PQ, Bi, col_len, nslices, st)
+                          : launch_cols_conv_tma_t<M, false, 1, false, true>(T, PQ, Bi, col_len, nslices, st);
       default: break;
     }
   }
