@@ -95,6 +95,51 @@ int tf_energy_fid(const float* d_fn, const float* d_fn_hi, const float* d_f, con
                   int three_d, double sigma, double p, double q, double T, const double* weights3,
                   double* d_ws, double* d_out3, void* stream);
 
+/* ---- NUFFT back-projection / FBP (K7, K8) --------------------------------
+ * Replaces radon._back_project_rows (radon.py:124-128), ramp_filter_apply
+ * (radon.py:137-142), fbp (radon.py:145-160) and nufft.type1 (nufft.py:203-223).
+ *
+ * tf_detector_rows: one DFT of length nd (<= 8192, any factorisation) per row of
+ *   d_rows [nrows][nd] fp32.  mode 0: d_out = complex64 [nrows][nd] polar
+ *   samples in signed-frequency order, sample jj of row i multiplied by
+ *   d_sphase[(i % n_angles) * nd + jj] (complex64), by |w_j| if ramp, and by
+ *   scale.  mode 1: d_out = fp32 [nrows][nd] ramp-filtered rows (x |w|, inverse
+ *   DFT, real part) times scale; d_sphase unused. */
+int tf_detector_rows(const float* d_rows, long long nrows, int nd, int n_angles,
+                     const void* d_sphase, int mode, int ramp, float scale, void* d_out,
+                     void* stream);
+
+/* Bytes of workspace tf_nufft_type1 needs per pass of `nslices` slices on an
+ * os x os grid (it chunks over slices when given less, down to one). */
+long long tf_nufft_workspace_bytes(int os, long long nslices);
+
+/* Type-1 NUFFT of nslices sample vectors (d_samples complex64, slice stride
+ * sample_stride) onto the N x N grid, by Kaiser-Bessel gridding of width
+ * `width` on an os x os grid (os a power of two, 32 <= os <= 8192, os >= 2N):
+ *   d_tile_ptr / d_tile_idx : int32 CSR of the samples touching each 32 x 32
+ *                             grid tile (tile = tb * (os/32) + ta), ascending
+ *   d_ab     : int32 [S][2] first window index (x, y), in [0, os)
+ *   d_wts    : fp32 [S][2*width] Kaiser-Bessel weights (x taps, then y taps)
+ *   d_prephase: complex64 [os] = e^{-2 pi i a (N/2) / os}
+ *   d_deapod : fp32 [N] deapodisation
+ * d_out = scale * deapod[ix] deapod[iy] * (inverse grid FFT)[ix][iy]:
+ * fp32 real part, or complex64 when out_complex.  Deterministic. */
+int tf_nufft_type1(const void* d_samples, long long sample_stride, long long nslices, int n,
+                   int os, int width, const int* d_tile_ptr, const int* d_tile_idx,
+                   const void* d_ab, const float* d_wts, const void* d_prephase,
+                   const float* d_deapod, float scale, int out_complex, void* d_out, void* d_ws,
+                   long long ws_bytes, void* stream);
+
+/* ---- Lanczos-3 resampling (K9) ----------------------------------------------
+ * One axis of the separable upsampler of multires.upsample (multires.py:145-195):
+ *   d_out[o][t][i] = sum_{k < taps} d_weights[t][k] * d_in[o][d_start[t] + k][i]
+ * for o < outer, t < n_tgt, i < inner (d_in is [outer][n_src][inner] fp32).
+ * d_start (int32 [n_tgt]) / d_weights (fp32 [n_tgt][taps], taps <= 8) are the
+ * band of the reference's edge-clamped, row-normalised interpolation matrix. */
+int tf_resample_axis(const float* d_in, float* d_out, long long outer, int n_src, int n_tgt,
+                     long long inner, const int* d_start, const float* d_weights, int taps,
+                     void* stream);
+
 /* Per-kernel CUDA-event timing used by bench.py for the roofline numbers.
  * Enable (clears totals), run, then collect: ms_out[slot] = total ms and
  * n_out[slot] = launches per slot (0 k_rows_fwd, 1 k_cols_conv, 2 k_rows_inv). */

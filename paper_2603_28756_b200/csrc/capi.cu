@@ -113,6 +113,15 @@ int energy_fid(const float* fn, const float* fn_hi, const float* f, const float*
                double* partial, double* out3, cudaStream_t st);
 int dot2(const float* x, const float* a, const float* b, long long n, double* out, double* ws,
          cudaStream_t st);
+size_t nufft_workspace_bytes(int os, long long nslices);
+int resample_axis(const float* in, float* out, long long outer, int n_src, int n_tgt,
+                  long long inner, const int* s0, const float* w, int K, cudaStream_t st);
+int detector_rows(const float* rows, long long nrows, int nd, int n_angles, const void* sph,
+                  int mode, int ramp, float scale, void* out, cudaStream_t st);
+int nufft_type1(const void* samples, long long s_stride, long long nslices, int n, int os, int w,
+                const int* tile_ptr, const int* tile_idx, const void* ab, const float* wts,
+                const void* preph, const float* deapod, float scale, int cplx, void* out,
+                void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace tf
 
@@ -217,6 +226,50 @@ int tf_energy_fid(const float* d_fn, const float* d_fn_hi, const float* d_f, con
   if (d_f && (!d_Kf || !d_Kfn)) return fail_arg("increment needs Kf and Kf_new");
   return energy_fid(d_fn, d_fn_hi, d_f, d_Kfn, d_Kf, d_rstar, nz, h, w, with_prior, three_d, sigma, p,
                     q, T, weights3, d_ws, d_out3, (cudaStream_t)stream);
+}
+
+long long tf_nufft_workspace_bytes(int os, long long nslices) {
+  if (os < 1 || nslices < 0) return fail_arg("bad NUFFT workspace query");
+  return (long long)nufft_workspace_bytes(os, nslices);
+}
+
+int tf_detector_rows(const float* d_rows, long long nrows, int nd, int n_angles,
+                     const void* d_sphase, int mode, int ramp, float scale, void* d_out,
+                     void* stream) {
+  TF_TRY(ensure_init());
+  if (nrows < 0 || !d_rows || !d_out) return fail_arg("bad tf_detector_rows arguments");
+  if (mode != 0 && mode != 1) return fail_arg("mode must be 0 (samples) or 1 (ramp rows)");
+  if (nrows == 0) return TF_OK;
+  return detector_rows(d_rows, nrows, nd, n_angles, d_sphase, mode, ramp, scale, d_out,
+                       (cudaStream_t)stream);
+}
+
+int tf_nufft_type1(const void* d_samples, long long sample_stride, long long nslices, int n,
+                   int os, int width, const int* d_tile_ptr, const int* d_tile_idx,
+                   const void* d_ab, const float* d_wts, const void* d_prephase,
+                   const float* d_deapod, float scale, int out_complex, void* d_out, void* d_ws,
+                   long long ws_bytes, void* stream) {
+  TF_TRY(ensure_init());
+  if (nslices < 0 || n < 1) return fail_arg("bad NUFFT shape");
+  if (nslices == 0) return TF_OK;
+  if (!d_samples || !d_tile_ptr || !d_tile_idx || !d_ab || !d_wts || !d_prephase || !d_deapod ||
+      !d_out || !d_ws)
+    return fail_arg("null pointer");
+  return nufft_type1(d_samples, sample_stride, nslices, n, os, width, d_tile_ptr, d_tile_idx, d_ab,
+                     d_wts, d_prephase, d_deapod, scale, out_complex, d_out, d_ws,
+                     (size_t)ws_bytes, (cudaStream_t)stream);
+}
+
+int tf_resample_axis(const float* d_in, float* d_out, long long outer, int n_src, int n_tgt,
+                     long long inner, const int* d_start, const float* d_weights, int taps,
+                     void* stream) {
+  TF_TRY(ensure_init());
+  if (outer < 0 || n_src < 1 || n_tgt < 1 || inner < 1 || taps < 1)
+    return fail_arg("bad resampling shape");
+  if (!d_in || !d_out || !d_start || !d_weights) return fail_arg("null pointer");
+  if (d_in == d_out) return fail_arg("in-place resampling is not supported");
+  return resample_axis(d_in, d_out, outer, n_src, n_tgt, inner, d_start, d_weights, taps,
+                       (cudaStream_t)stream);
 }
 
 int tf_timing_enable(int on) {

@@ -1,0 +1,77 @@
+"""CUDA Lanczos upsampler and the GPU coarse-to-fine driver vs reference fixtures."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tf():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_28756_b200 as m
+
+    return m
+
+
+def test_upsample_matches_reference(tf):
+    d = golden("multires.npz")
+    assert rel_l2(tf.upsample(d["v"], 20, 6), d["up3"]) < 1e-6
+    assert rel_l2(tf.upsample(d["v"][0], 25), d["up2"]) < 1e-6
+    g = tf.upsample(tf.ImageGrid(d["v"][0]), 25)
+    assert isinstance(g, tf.ImageGrid) and rel_l2(g.data, d["up2"]) < 1e-6
+
+
+def test_upsample_identity_and_constants(tf):
+    """test_multires.py:99-119"""
+    x = np.random.default_rng(1).standard_normal((4, 16, 16))
+    np.testing.assert_allclose(tf.upsample(x, 16, 4), x, rtol=0, atol=1e-6)
+    c = tf.upsample(np.full((3, 8, 8), 2.5), 32, 6)
+    np.testing.assert_allclose(c, 2.5, rtol=1e-6)
+
+
+def test_upsample_c3_level_vs_oracle(tf):
+    """(Z/2, 1024^2) -> (Z, 2048^2), the C3 level transfer, on a 4-slice slab."""
+    import oracle as O
+
+    x = np.random.default_rng(2).standard_normal((2, 1024, 1024))
+    ref = O.upsample(x, 2048, 4)
+    assert rel_l2(tf.upsample(x, 2048, 4), ref) < 1e-6
+
+
+def test_solve_hierarchical_matches_reference(tf):
+    d = golden("hier.npz")
+    sino = tf.Sinogram(angles=d["angles"], data=d["g"])
+    prm = tf.QggmrfParams(sigma=0.1, lam=1e-2)
+    hier = tf.GridHierarchy(levels=(16, 32), iters_per_level=(6, 4))
+    seen = []
+    est, lrecs = tf.solve_hierarchical(sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300),
+                                       use_fbp_init=True, on_record=lambda l, r: seen.append(l))
+    assert isinstance(est, tf.Volume)
+    assert rel_l2(est.data, d["recon"]) < 1e-3
+    np.testing.assert_allclose([r.objective for r in lrecs[0]], d["obj0"], rtol=1e-4)
+    np.testing.assert_allclose([r.objective for r in lrecs[1]], d["obj1"], rtol=1e-4)
+    assert seen == [0] * 7 + [1] * 5
+
+
+def test_single_level_equals_plain_solve(tf):
+    """test_multires.py:168-179: one level == fidelity_context + solve."""
+    import torch
+
+    d = golden("solve_3d.npz")
+    n = d["f0"].shape[1]
+    sino = tf.Sinogram(angles=d["angles"], data=d["g"])
+    prm = tf.QggmrfParams(sigma=float(d["sigma"]), lam=float(d["lam"]))
+    cfg = tf.SolverConfig(max_iters=5, tol=1e-300, lipschitz=float(d["L"]))
+    est, _ = tf.solve_hierarchical(sino, tf.GridHierarchy(levels=(n,), iters_per_level=(5,)), prm,
+                                   cfg)
+    geom = tf.ScanGeometry(angles=d["angles"], detector_bins=d["g"].shape[2], image_side=n)
+    p = tf.NufftPlan(n, tf.polar_sampling(geom), 1e-6)
+    ctx = tf.fidelity_context(p, tf.build_psf(p.sampling, n), sino)
+    rec, _ = tf.solve(ctx, prm, cfg, torch.zeros((d["g"].shape[0], n, n), device="cuda"))
+    np.testing.assert_array_equal(est.data, rec.double().cpu().numpy())
