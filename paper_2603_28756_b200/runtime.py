@@ -1,0 +1,296 @@
+"""z-slab parallel MBIR: one process per GPU, NCCL halo exchange + scalar allreduce.
+
+Drop-in for the slab runtime of tomoforge/runtime.py: ``SlabPartition`` /
+``partition`` (runtime.py:82-125), ``exchange_halos`` (:345-367) and
+``distributed_solve`` (:622-691) with the worker loop of :523-619.
+
+The reference runs one thread per slab and models MPI with queue/socket
+transports.  Here every slab is a process bound to one GPU (torchrun), and the
+protocol is carried by ``torch.distributed``:
+
+* per iteration exactly one halo exchange: each rank sends its first plane of
+  the new iterate to the lower neighbour and its last plane to the upper one
+  (contiguous N^2 fp32 planes -- no packing), 2 (W-1) messages in total,
+  NCCL send/recv straight from device memory (``batch_isend_irecv``); on a
+  gloo group the planes are staged through host memory;
+* one allreduce of three fp64 scalars [energy, fidelity increment, ||grad||^2],
+  so every rank takes the identical restart / stop decision
+  (runtime.py:581-588; the sum is bitwise identical on all ranks);
+* the extrapolated point's halos are never sent: the fused K4 kernel forms
+  y = f + c (f - f_prev) on the fly, halo planes included (runtime.py:590-597);
+* the fidelity term is slice-local, so the Toeplitz apply and R*g need no
+  communication (runtime.py:5-6).
+
+The objective bookkeeping is the single-GPU solver's (solver.py): increments
+accumulated in fp64 and reduced across ranks.
+"""
+
+from __future__ import annotations
+
+import collections
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .geometry import ScanGeometry, Sinogram, Volume, polar_sampling
+from .nufft import NufftPlan
+from .qggmrf import stencil_2d, stencil_3d
+from .radon import back_project_stack
+from .solver import SolverConfig, _iterate, estimate_lipschitz, solve
+from .toeplitz import FidelityContext, build_psf, fidelity_context
+
+__all__ = [
+    "SlabPartition",
+    "TransportError",
+    "ProtocolError",
+    "TransportTimeout",
+    "SlabComm",
+    "partition",
+    "exchange_halos",
+    "distributed_solve",
+]
+
+
+class TransportError(RuntimeError):
+    pass
+
+
+class ProtocolError(TransportError):
+    """A slab or plane does not match the partition it is exchanged under."""
+
+
+class TransportTimeout(TransportError):
+    """An expected neighbour message never arrived (collective timeout)."""
+
+
+@dataclass(frozen=True)
+class SlabPartition:
+    """Contiguous slice range [begin, end) owned by one worker (runtime.py:82-105)."""
+
+    worker_id: int
+    begin: int
+    end: int
+    lower: int | None
+    upper: int | None
+    halo_width: int = 1
+
+    def __post_init__(self):
+        if self.end <= self.begin:
+            raise ValueError("empty slab")
+        if self.halo_width != 1:
+            raise ValueError("halo width is fixed at 1 (26-neighbor stencil reach)")
+
+    @property
+    def slice_range(self):
+        return (self.begin, self.end)
+
+    @property
+    def size(self) -> int:
+        return self.end - self.begin
+
+
+def partition(n_slices: int, n_workers: int) -> list[SlabPartition]:
+    """Balanced contiguous slabs, sizes differ by at most 1, larger first (runtime.py:108-125)."""
+    if n_workers < 1:
+        raise ValueError("need at least one worker")
+    if n_slices < n_workers:
+        raise ValueError(f"cannot split {n_slices} slices across {n_workers} workers")
+    base, extra = divmod(n_slices, n_workers)
+    parts, begin = [], 0
+    for w in range(n_workers):
+        size = base + (1 if w < extra else 0)
+        parts.append(SlabPartition(worker_id=w, begin=begin, end=begin + size,
+                                   lower=w - 1 if w > 0 else None,
+                                   upper=w + 1 if w < n_workers - 1 else None))
+        begin += size
+    return parts
+
+
+def exchange_halos(partitions, slabs, iteration: int = 0, transport=None):
+    """Driver-side bulk exchange over all slabs held by one process (runtime.py:345-367):
+    one ``(halo_lo, halo_hi)`` per slab, ``None`` on open ends.  The lower halo is
+    the lower neighbour's last plane, the upper halo the upper neighbour's first."""
+    if len(partitions) != len(slabs):
+        raise ValueError("need exactly one slab per partition")
+    for part, slab in zip(partitions, slabs):
+        if slab.shape[0] != part.size:
+            raise ValueError(f"slab of worker {part.worker_id} has {slab.shape[0]} slices, "
+                             f"expected {part.size}")
+    out = []
+    for part in partitions:
+        lo = slabs[part.lower][-1] if part.lower is not None else None
+        hi = slabs[part.upper][0] if part.upper is not None else None
+        out.append((lo, hi))
+    return out
+
+
+class SlabComm:
+    """This rank's end of the slab protocol over a torch.distributed group.
+
+    ``exchange(slab)`` returns the (lower, upper) halo planes of ``slab`` (None on
+    open ends); ``allreduce(values)`` sums a short fp64 vector.  ``counts`` keeps
+    per-purpose message counts (the reference's protocol budget,
+    test_runtime.py:239-250).
+    """
+
+    def __init__(self, part: SlabPartition, group=None):
+        self.part = part
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.rank != part.worker_id:
+            raise ProtocolError(f"rank {self.rank} given the partition of worker {part.worker_id}")
+        self.direct = dist.get_backend(group) == "nccl"
+        self.counts = collections.Counter()
+
+    def _peer(self, w):
+        return w if self.group is None else dist.get_global_rank(self.group, w)
+
+    def exchange(self, slab: torch.Tensor):
+        part = self.part
+        if slab.shape[0] != part.size:
+            raise ProtocolError(f"slab has {slab.shape[0]} slices, partition owns {part.size}")
+        plane_shape = slab.shape[1:]
+        staged = not (self.direct and slab.is_cuda)
+        buf_dev = "cpu" if staged else slab.device
+        ops, lo, hi = [], None, None
+
+        def out(t):
+            return t.to("cpu") if staged else t
+
+        if part.lower is not None:
+            lo = torch.empty(plane_shape, dtype=slab.dtype, device=buf_dev)
+            ops.append(dist.P2POp(dist.isend, out(slab[0]).contiguous(), self._peer(part.lower),
+                                  self.group))
+            ops.append(dist.P2POp(dist.irecv, lo, self._peer(part.lower), self.group))
+            self.counts["halo"] += 1
+        if part.upper is not None:
+            hi = torch.empty(plane_shape, dtype=slab.dtype, device=buf_dev)
+            ops.append(dist.P2POp(dist.isend, out(slab[-1]).contiguous(), self._peer(part.upper),
+                                  self.group))
+            ops.append(dist.P2POp(dist.irecv, hi, self._peer(part.upper), self.group))
+            self.counts["halo"] += 1
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if staged and slab.is_cuda:
+            lo = lo.to(slab.device) if lo is not None else None
+            hi = hi.to(slab.device) if hi is not None else None
+        return lo, hi
+
+    def allreduce(self, values: torch.Tensor) -> torch.Tensor:
+        """Sum of an fp64 vector over the group (identical on every rank)."""
+        t = values.to(torch.float64)
+        if not (self.direct and t.is_cuda):
+            t = t.cpu()
+        t = t.clone()
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        self.counts["reduce"] += 1
+        return t
+
+    def broadcast_scalar(self, value: float | None, root: int = 0) -> float:
+        dev = torch.device("cuda", torch.cuda.current_device()) if self.direct else "cpu"
+        t = torch.tensor([value if value is not None else 0.0], dtype=torch.float64, device=dev)
+        dist.broadcast(t, src=self._peer(root), group=self.group)
+        return float(t.item())
+
+    def gather(self, slab: torch.Tensor, parts, root: int = 0):
+        """Full volume on ``root`` (None elsewhere); slabs padded to the largest size."""
+        big = max(p.size for p in parts)
+        dev = slab.device if (self.direct and slab.is_cuda) else torch.device("cpu")
+        pad = torch.zeros((big,) + tuple(slab.shape[1:]), dtype=slab.dtype, device=dev)
+        pad[:slab.shape[0]] = slab.to(dev)
+        bufs = [torch.empty_like(pad) for _ in range(self.world)] if self.rank == root else None
+        dist.gather(pad, bufs, dst=self._peer(root), group=self.group)
+        self.counts["gather"] += 1
+        if self.rank != root:
+            return None
+        return torch.cat([bufs[p.worker_id][:p.size] for p in parts])
+
+
+def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig, n_workers: int,
+                      *, f0: Volume | None = None, transport=None, nufft_tolerance: float = 1e-6,
+                      oversampling: float = 2.0, on_record=None, snapshot_sink=None,
+                      gather: str = "root", group=None):
+    """Slab-parallel reconstruction, algebraically identical to ``solve`` (runtime.py:622-691).
+
+    SPMD: every rank of the process group (one per GPU, ``n_workers`` = group
+    size) calls it with the same arguments and reconstructs its own slab.
+    Returns ``(volume, records)``: with ``gather="root"`` rank 0 gets the full
+    ``Volume`` and other ranks ``None``; with ``gather="none"`` every rank gets its
+    own slab as a device tensor.  ``on_record`` / ``snapshot_sink`` fire on rank
+    0 only (snapshots gather the full volume every iteration -- tests only).
+    ``transport`` is accepted for signature compatibility; the transport is the
+    process group.
+    """
+    if n_workers < 1:
+        raise ValueError("need at least one worker")
+    if n_workers > sino.slices:
+        raise ValueError("more workers than slices")
+    if gather not in ("root", "none"):
+        raise ValueError("gather must be 'root' or 'none'")
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if n_workers != world and not (n_workers == 1 and world == 1):
+        raise ValueError(f"n_workers={n_workers} must equal the process-group size {world} "
+                         "(one process per GPU; launch with torchrun)")
+    geom = ScanGeometry(angles=sino.angles, detector_bins=sino.detector_bins,
+                        image_side=image_side)
+    sampling = polar_sampling(geom)
+    plan = NufftPlan(image_side, sampling, nufft_tolerance, oversampling)
+    psf = build_psf(sampling, image_side, nufft_tolerance, oversampling)
+    if f0 is not None and (f0.slices != sino.slices or f0.side != image_side):
+        raise ValueError("initial volume does not match the requested reconstruction")
+
+    if n_workers == 1:
+        L = cfg.lipschitz if cfg.lipschitz is not None else estimate_lipschitz(psf, params)
+        cfg1 = SolverConfig(max_iters=cfg.max_iters, tol=cfg.tol, lipschitz=L,
+                            restart=cfg.restart, log_every=cfg.log_every, nonneg=cfg.nonneg)
+        ctx = fidelity_context(plan, psf, sino)
+        x0 = f0 if f0 is not None else torch.zeros((sino.slices, image_side, image_side),
+                                                   device=_lib.device())
+        vol, records = solve(ctx, params, cfg1, x0, on_record=on_record,
+                             snapshot_sink=snapshot_sink)
+        if isinstance(vol, torch.Tensor):
+            if gather == "none":
+                return vol, records
+            vol = Volume(vol.to("cpu", torch.float64).numpy())
+        return vol, records
+
+    rank = dist.get_rank(group)
+    parts = partition(sino.slices, n_workers)
+    part = parts[rank]
+    comm = SlabComm(part, group)
+    try:
+        L = cfg.lipschitz
+        if L is None:
+            L = comm.broadcast_scalar(estimate_lipschitz(psf, params) if rank == 0 else None)
+        rows = sino.data[part.begin:part.end]
+        ctx = FidelityContext(psf=psf, rstar=back_project_stack(plan, rows),
+                              g_norm_sq=float(np.sum(rows ** 2)))
+        if f0 is None:
+            x0 = torch.zeros((part.size, image_side, image_side), device=_lib.device())
+        else:
+            x0 = torch.from_numpy(np.ascontiguousarray(f0.data[part.begin:part.end],
+                                                       dtype=np.float32)).to(_lib.device())
+        stencil = stencil_3d() if sino.slices > 1 else stencil_2d()
+        sink = None
+        if snapshot_sink is not None:
+            def sink(k, slab):
+                full = comm.gather(slab, parts)
+                if rank == 0:
+                    snapshot_sink(k, full.to("cpu", torch.float64).numpy())
+        slab, records = _iterate(ctx, params, cfg, x0, stencil, L, comm=comm,
+                                 on_record=on_record if rank == 0 else None,
+                                 device_snapshot=sink)
+        if gather == "none":
+            return slab, records
+        full = comm.gather(slab, parts)
+        vol = Volume(full.to("cpu", torch.float64).numpy()) if rank == 0 else None
+        return vol, records
+    except (TransportError, ValueError, FloatingPointError):
+        raise
+    except Exception as exc:  # noqa: BLE001 - same contract as runtime.py:688-690
+        raise RuntimeError(f"worker {rank} failed: {exc}") from exc

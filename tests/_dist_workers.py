@@ -1,0 +1,59 @@
+"""Multi-process workers for the runtime tests (spawned with torch.multiprocessing)."""
+
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def _init(rank, world, port, backend="gloo"):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+
+
+def comm_worker(rank, world, port, n_slices, side, out_dir):
+    """Exchange / allreduce / gather of the slab protocol on CPU tensors (gloo)."""
+    from paper_2603_28756_b200.runtime import SlabComm, partition
+
+    _init(rank, world, port)
+    try:
+        parts = partition(n_slices, world)
+        part = parts[rank]
+        full = np.arange(n_slices * side * side, dtype=np.float32).reshape(n_slices, side, side)
+        slab = torch.from_numpy(full[part.begin:part.end].copy())
+        comm = SlabComm(part)
+        lo, hi = comm.exchange(slab)
+        red = comm.allreduce(torch.tensor([1.0, float(rank), float(part.size)], dtype=torch.float64))
+        g = comm.gather(slab, parts)
+        res = {"lo": None if lo is None else lo.numpy(), "hi": None if hi is None else hi.numpy(),
+               "red": red.numpy(), "halo_msgs": comm.counts["halo"]}
+        if rank == 0:
+            res["gather"] = g.numpy()
+        np.save(os.path.join(out_dir, f"rank{rank}.npy"), res, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def solve_worker(rank, world, port, fixture, out_dir):
+    """distributed_solve on cuda:0 with a gloo group (host-staged halos)."""
+    import paper_2603_28756_b200 as tf
+    from paper_2603_28756_b200.runtime import distributed_solve
+
+    torch.cuda.set_device(0)
+    _init(rank, world, port)
+    try:
+        d = dict(np.load(fixture))
+        sino = tf.Sinogram(angles=d["angles"], data=d["g"])
+        prm = tf.QggmrfParams(sigma=0.3, lam=0.05)
+        cfg = tf.SolverConfig(max_iters=8, tol=1e-300, lipschitz=None)
+        snaps = []
+        vol, recs = distributed_solve(sino, 16, prm, cfg, world,
+                                      snapshot_sink=lambda k, v: snaps.append(v))
+        if rank == 0:
+            np.save(os.path.join(out_dir, "solve.npy"),
+                    {"vol": vol.data, "obj": np.array([r.objective for r in recs]),
+                     "nsnap": len(snaps)}, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
