@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-mbir", action="store_true")
     return ap.parse_args()
 
 
@@ -282,6 +283,10 @@ def run_ours(args, world, rank, local):
     e2e = None
     if not args.no_e2e:
         e2e = _e2e(tf, ctx, z, world, args.e2e_steps)
+    mbir = None
+    if not args.no_mbir:
+        del out
+        mbir = _mbir(tf, args, world, rank)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         _, _, _, threads, slices, times = cpu_sample()
@@ -295,7 +300,7 @@ def run_ours(args, world, rank, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: randn volume, R*g from a randn sinogram",
             "config": config(args, world), "roofline": roofline, "cpu_baseline": cpu,
-            "e2e": e2e, "gpu_launches": launches,
+            "e2e": e2e, "gpu_launches": launches, "mbir": mbir,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -334,8 +339,65 @@ def _e2e(tf, ctx, z, world, steps):
     dt = max_over_ranks(dt, world)
     assert out.shape == f.shape
     return {"value": z * world * steps / dt, "unit": UNIT,
-            "h2d_bytes_per_step": int(f.size * 4), "d2h_bytes_per_step": int(f.size * 4),
+            "h2d_bytes_per_step": int(f.nbytes), "d2h_bytes_per_step": int(f.nbytes),
             "api": "fidelity_grad(ctx, numpy float64 (64, 2048, 2048)) -> numpy float64"}
+
+
+def _mbir(tf, args, world, rank):
+    """Full MBIR on the C3 slab (configs[2]): one-time setup, per-iteration solver time
+    at the finest level, and the 3-level (512, 1024, 2048) x (40, 20, 10) schedule end
+    to end.  Synthetic randn sinogram (timing does not depend on the values)."""
+    import torch
+
+    from paper_2603_28756_b200.radon import fbp_stack
+
+    z = args.slices
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = np.random.default_rng(4000 + rank).standard_normal((z, N_ANGLES, N_BINS))
+    sino = tf.Sinogram(angles=angles(), data=g)
+    prm = tf.QggmrfParams(sigma=0.5, lam=5e-4)
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = fn()
+        b.record()
+        torch.cuda.synchronize()
+        return r, max_over_ranks(a.elapsed_time(b), world)
+
+    geom = tf.ScanGeometry(angles=angles(), detector_bins=N_BINS, image_side=N_SIDE)
+    plan = tf.NufftPlan(N_SIDE, tf.polar_sampling(geom), 1e-6)
+    plan.device_tables()  # host-side plan tables, not GPU work
+    psf, t_psf = timed(lambda: tf.build_psf(plan.sampling, N_SIDE))
+    ctx, t_rstar = timed(lambda: tf.fidelity_context(plan, psf, sino))
+    f0, t_fbp = timed(lambda: fbp_stack(plan, g))
+    L = tf.estimate_lipschitz(psf, prm)
+    iters = 10
+    cfg = tf.SolverConfig(max_iters=iters, tol=1e-300, lipschitz=L)
+    tf.solve(ctx, prm, tf.SolverConfig(max_iters=2, tol=1e-300, lipschitz=L), f0)  # warm
+    _, t_solve = timed(lambda: tf.solve(ctx, prm, cfg, f0))
+    per_it = t_solve / iters
+    vox = z * N_SIDE * N_SIDE
+    # bytes per voxel-iteration: Toeplitz 44 (DESIGN §3) + K4 24 + K5 20 (DESIGN §4)
+    bpv = 88.0
+    peak = _peak_hbm()["value"]
+    del ctx, f0
+    torch.cuda.empty_cache()
+    hier = tf.GridHierarchy(levels=(512, 1024, 2048), iters_per_level=(40, 20, 10))
+    _, t_hier = timed(lambda: tf.solve_hierarchical(
+        sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300, lipschitz=L), use_fbp_init=True))
+    return {
+        "workload": f"C3 slab: {z} x 2048^2 per GPU, 128 angles, Nd=2048, qGGMRF lam=5e-4",
+        "setup_ms": {"psf": t_psf, "rstar_nufft": t_rstar, "fbp_nufft": t_fbp},
+        "solve_ms_per_iter": per_it,
+        "solve_bytes_per_voxel_iter": bpv,
+        "solve_hbm_frac": bpv * vox / (per_it / 1e3) / 1e9 / peak,
+        "hierarchical_3level_ms": t_hier,
+        "hierarchical_schedule": "levels (512, 1024, 2048), iterations (40, 20, 10), FBP init, "
+                                 "Lanczos-3 upsampling, L fixed from the finest level",
+    }
 
 
 def _peak_hbm():

@@ -64,10 +64,38 @@ def as_stack(f, what: str = "input"):
     raise ValueError(f"{what} must be 2D or 3D, got shape {arr.shape}")
 
 
+_CHUNK_ELEMS = 1 << 25  # 256 MB of float64 per staged copy
+
+
 def to_device(arr: np.ndarray) -> torch.Tensor:
-    """float64 host array -> contiguous fp32 device tensor (pinned staging)."""
-    host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32))
-    return host.to(_lib.device(), non_blocking=False)
+    """float64 (or any real) host array -> contiguous fp32 device tensor.
+
+    The host array is copied as is (no host-side conversion pass) in chunks of
+    256 MB and narrowed to fp32 on the device."""
+    arr = np.ascontiguousarray(arr)
+    dev = _lib.device()
+    if arr.dtype == np.float32:
+        return torch.from_numpy(arr).to(dev)
+    if arr.dtype != np.float64:
+        arr = arr.astype(np.float64)
+    out = torch.empty(arr.shape, dtype=torch.float32, device=dev)
+    src = torch.from_numpy(arr).reshape(-1)
+    dst = out.reshape(-1)
+    for lo in range(0, src.numel(), _CHUNK_ELEMS):
+        hi = min(src.numel(), lo + _CHUNK_ELEMS)
+        dst[lo:hi].copy_(src[lo:hi].to(dev))
+    return out
+
+
+def to_host64(t: torch.Tensor) -> np.ndarray:
+    """fp32 device tensor -> float64 host array (widened on the device, chunked)."""
+    out = np.empty(tuple(t.shape), dtype=np.float64)
+    dst = torch.from_numpy(out).reshape(-1)
+    src = t.detach().reshape(-1)
+    for lo in range(0, src.numel(), _CHUNK_ELEMS):
+        hi = min(src.numel(), lo + _CHUNK_ELEMS)
+        dst[lo:hi].copy_(src[lo:hi].to(torch.float64))
+    return out
 
 
 def wrap_like(kind: str, t: torch.Tensor):
@@ -76,7 +104,7 @@ def wrap_like(kind: str, t: torch.Tensor):
         return t
     if kind == "tensor2":
         return t[0]
-    host = t.detach().to("cpu", torch.float64).numpy()
+    host = to_host64(t)
     if kind == "image":
         return ImageGrid(host[0])
     if kind == "volume":

@@ -1,47 +1,82 @@
-"""Build the in-tree C-ABI library with nvcc for sm_100a (no JIT, no torch extension)."""
+"""Build the in-tree C-ABI library with nvcc for sm_100a (no JIT, no torch extension).
+
+Each ``csrc/*.cu`` is its own translation unit, compiled in parallel
+(``-gencode arch=compute_100a,code=sm_100a -lineinfo``) and linked into
+``libtomoforge_b200.so``.  Objects go to ``build/`` (git-ignored).
+"""
 
 from __future__ import annotations
 
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libtomoforge_b200.so"
+OBJ = HERE.parent / "build" / "obj"
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-shared", "-Xcompiler", "-fPIC",
+    "-Xcompiler", "-fPIC",
 ]
 
 
-def sources():
-    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh"))
+def units():
+    return sorted(CSRC.glob("*.cu"))
+
+
+def headers():
+    return sorted(CSRC.glob("*.cuh"))
 
 
 def up_to_date() -> bool:
     if not LIB.exists():
         return False
     t = LIB.stat().st_mtime
-    return all(p.stat().st_mtime <= t for p in sources())
+    return all(p.stat().st_mtime <= t for p in units() + headers() + [Path(__file__)])
+
+
+def _compile(nvcc: str, src: Path, verbose: bool):
+    obj = OBJ / (src.stem + ".o")
+    newest_dep = max(p.stat().st_mtime for p in [src] + headers() + [Path(__file__)])
+    if obj.exists() and obj.stat().st_mtime >= newest_dep:
+        return obj, None
+    cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if res.returncode != 0:
+        return obj, f"{src.name}: nvcc failed ({res.returncode})\n{res.stdout}{res.stderr}"
+    if verbose:
+        sys.stderr.write(res.stderr)
+    return obj, None
 
 
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, str(CSRC / "lib.cu"), "-o", str(LIB) + ".tmp"]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    OBJ.mkdir(parents=True, exist_ok=True)
+    if force:
+        for o in OBJ.glob("*.o"):
+            o.unlink()
+    with ThreadPoolExecutor(max_workers=len(units())) as ex:
+        results = list(ex.map(lambda s: _compile(nvcc, s, verbose), units()))
+    errors = [e for _, e in results if e]
+    if errors:
+        sys.stderr.write("\n".join(errors))
+        raise RuntimeError("nvcc failed")
+    objs = [str(o) for o, _ in results]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o",
+           str(LIB) + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode})")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError(f"nvcc link failed ({res.returncode})")
     os.replace(str(LIB) + ".tmp", LIB)
     return LIB
 

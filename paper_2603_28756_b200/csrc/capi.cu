@@ -65,7 +65,8 @@ static std::mutex g_init_mu;
 static std::vector<int> g_inited;  // per device ordinal
 static std::vector<int> g_sms;
 
-int init_twiddles();
+int init_twiddles_toeplitz();
+int init_twiddles_nufft();
 
 int ensure_init() {
   int dev = 0;
@@ -76,7 +77,8 @@ int ensure_init() {
     g_sms.resize(dev + 1, 0);
   }
   if (!g_inited[dev]) {
-    TF_TRY(init_twiddles());
+    TF_TRY(init_twiddles_toeplitz());
+    TF_TRY(init_twiddles_nufft());
     int sms = 0;
     TF_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev),
                       "cudaDeviceGetAttribute"));

@@ -380,6 +380,8 @@ int dispatch_grid_fft(int os, const c32* grid, c32* Tn, long long nz, int n, con
 
 }  // namespace
 
+int init_twiddles_nufft() { return check_cuda(init_twiddles_tu(), "twiddle init (nufft)"); }
+
 size_t nufft_workspace_bytes(int os, long long nslices) {
   const size_t plane = (size_t)os * os * sizeof(c32);
   return (size_t)nslices * (plane + plane / 2);

@@ -26,42 +26,73 @@ namespace tf {
 struct PriorConsts {
   float inv_sp;      // 1 / sigma^p
   float inv_psp;     // 1 / (p sigma^p)
-  float log2_ts;     // log2(T sigma)
+  float c0;          // (p - q) log2(T sigma)
   float pq;          // p - q
   float qp;          // q / p
   float p;           // p
+  float pm1;         // p - 1
   float w[4];        // stencil weights by number of nonzero offset components (1, 2, 3)
 };
 
 constexpr int TX = 32, TY = 8;
+constexpr int HX = TX + 2, HY = TY + 2;  // tile with a one-voxel ring
+constexpr int HALO_ELEMS = HX * HY;       // 340: thread i loads elements i and i + 256
 
-// v = (|d| / (T sigma))^(p-q), via the SFU (lg2/ex2); v = 0 at d = 0
-__device__ __forceinline__ float qg_v(float ad, const PriorConsts& pc) {
-  return exp2f(pc.pq * (__log2f(ad) - pc.log2_ts));
+// MUFU transcendentals (log2 / exp2: one XU instruction each)
+__device__ __forceinline__ float lg2a(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2a(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
-// rho'(d) = sign(d) |d|^(p-1) / sigma^p * (1 + (q/p) v) / (1 + v)^2  (qggmrf.py:124-130)
-template <bool P2>
-__device__ __forceinline__ float rho_prime(float d, const PriorConsts& pc) {
-  const float ad = fabsf(d);
-  const float v = qg_v(ad, pc);
-  const float onev = 1.f + v;
-  const float shape = __fdividef(fmaf(pc.qp, v, 1.f), onev * onev);
-  float mag;
-  if constexpr (P2) mag = d;  // sign(d) |d|
-  else mag = copysignf(exp2f((pc.p - 1.f) * __log2f(ad)), d);
-  return mag * pc.inv_sp * shape;
+// 1/x for x >= 1 on the FMA pipe: integer seed (rel. error < 12.5 %) and three
+// Newton steps (error squares each step: < 4e-8), two lanes at a time.  Keeps
+// the XU free for log2/exp2, which bound these kernels.
+__device__ __forceinline__ float2 rcp2_ge1(float2 x) {
+  float2 y = mk(__int_as_float(0x7EF311C3 - __float_as_int(x.x)),
+                __int_as_float(0x7EF311C3 - __float_as_int(x.y)));
+  const float2 nx = mk(-x.x, -x.y), one = mk(1.f, 1.f);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) y = pfma(y, pfma(nx, y, one), y);
+  return y;
 }
 
-// rho(d) = |d|^p / (p sigma^p) / (1 + v)  (qggmrf.py:117-121)
+// v = (|d| / (T sigma))^(p-q) for two differences; t = log2|d| (v = 0 at d = 0)
+__device__ __forceinline__ float2 qg_v2(float2 d, float2& t, const PriorConsts& pc) {
+  t = mk(lg2a(fabsf(d.x)), lg2a(fabsf(d.y)));
+  const float2 e = pfma(mk(pc.pq, pc.pq), t, mk(-pc.c0, -pc.c0));
+  return mk(ex2a(e.x), ex2a(e.y));
+}
+
+// sigma^p rho'(d) = sign(d) |d|^(p-1) (1 + (q/p) v) / (1 + v)^2   (qggmrf.py:124-130)
 template <bool P2>
-__device__ __forceinline__ float rho(float d, const PriorConsts& pc) {
-  const float ad = fabsf(d);
-  const float v = qg_v(ad, pc);
-  float mag;
-  if constexpr (P2) mag = d * d;
-  else mag = exp2f(pc.p * __log2f(ad));
-  return __fdividef(mag * pc.inv_psp, 1.f + v);
+__device__ __forceinline__ float2 drho2(float2 d, const PriorConsts& pc) {
+  float2 t;
+  const float2 v = qg_v2(d, t, pc);
+  const float2 one = mk(1.f, 1.f);
+  const float2 r = rcp2_ge1(cadd(v, one));
+  const float2 s = pmul(pfma(mk(pc.qp, pc.qp), v, one), pmul(r, r));
+  float2 mag;
+  if constexpr (P2) mag = d;
+  else mag = mk(copysignf(ex2a(pc.pm1 * t.x), d.x), copysignf(ex2a(pc.pm1 * t.y), d.y));
+  return pmul(mag, s);
+}
+
+// p sigma^p rho(d) = |d|^p / (1 + v)   (qggmrf.py:117-121)
+template <bool P2>
+__device__ __forceinline__ float2 rho2(float2 d, const PriorConsts& pc) {
+  float2 t;
+  const float2 v = qg_v2(d, t, pc);
+  const float2 r = rcp2_ge1(cadd(v, mk(1.f, 1.f)));
+  float2 mag;
+  if constexpr (P2) mag = pmul(d, d);
+  else mag = mk(ex2a(pc.p * t.x), ex2a(pc.p * t.y));
+  return pmul(mag, r);
 }
 
 template <int NT>
@@ -93,45 +124,85 @@ struct Planes {
   }
 };
 
+// The two halo-tile elements a thread stages per plane, resolved once per CTA:
+// tile position and in-plane offset, or -1 outside the grid.
+struct HaloSlots {
+  int sm[2];
+  long long off[2];
+  __device__ __forceinline__ void init(int h, int w) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int e = threadIdx.x + k * TX * TY;
+      const int ly = e / HX, lx = e - ly * HX;
+      const int gx = blockIdx.y * TY + ly - 1, gy = blockIdx.x * TX + lx - 1;
+      sm[k] = e < HALO_ELEMS ? e : -1;
+      off[k] = (e < HALO_ELEMS && gx >= 0 && gx < h && gy >= 0 && gy < w) ? (long long)gx * w + gy
+                                                                          : -1;
+    }
+  }
+};
+
+// In-plane neighbour masks of voxel (ix, iy): weight * [neighbour inside the slice]
+struct InPlaneW {
+  float w8[9];  // index (dy+1)*3 + (dx+1): offsets in the same plane (centre unused)
+  float wz[9];  // the same (dy, dx) on the planes above/below (weight class + 1)
+  __device__ __forceinline__ void init(int ix, int iy, int h, int w, const PriorConsts& pc) {
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const bool ok = ix + dy >= 0 && ix + dy < h && iy + dx >= 0 && iy + dx < w;
+        const int k = (dy != 0) + (dx != 0);
+        w8[(dy + 1) * 3 + dx + 1] = ok ? pc.w[k] : 0.f;
+        wz[(dy + 1) * 3 + dx + 1] = ok ? pc.w[k + 1] : 0.f;
+      }
+  }
+};
+
 // ============================================================ K4
 // grad = K y - R*g + lam * grad_prior(y)   (Kf/Kfp/rstar may be null -> 0)
 // write_grad == 0: out = y - grad / L  [clamped at 0 if NONNEG]   (the update)
 // write_grad == 1: out = grad                                     (prior_grad API)
 // partial[block] = sum grad^2 over the block's voxels (fp64)
+// The 26 (3-D) or 8 (2-D) differences of a voxel are evaluated two at a time on
+// the paired-fp32 datapath; per pair the XU runs only log2 and exp2.
 template <bool THREE_D, bool P2, bool NONNEG>
 __global__ void __launch_bounds__(TX* TY)
 k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* __restrict__ Kfp,
                const float* __restrict__ rstar, float* __restrict__ f_new,
                double* __restrict__ partial, int nz, int h, int w, float c, float lam,
                float inv_L, int write_grad, PriorConsts pc) {
-  __shared__ float ys[3][TY + 2][TX + 2];
+  __shared__ float ys[3][HY][HX];
   __shared__ double red[TX * TY / 32];
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int iy = blockIdx.x * TX + tx;  // contiguous axis
   const int ix = blockIdx.y * TY + ty;
   const long long nn = (long long)h * w;
   const bool inside = ix < h && iy < w;
+  HaloSlots hs;
+  hs.init(h, w);
+  InPlaneW ipw;
+  ipw.init(ix, iy, h, w, pc);
+  float* ysf = &ys[0][0][0];
 
   // y on plane zz into ring slot s (0 outside the grid or on an invalid plane)
   auto load_plane = [&](int zz, int s) {
     const float* pf = F.at(zz, nz, nn);
     const float* pp = FP.at(zz, nz, nn);
-    for (int e = threadIdx.x; e < (TY + 2) * (TX + 2); e += TX * TY) {
-      const int ly = e / (TX + 2), lx = e - ly * (TX + 2);
-      const int gx = blockIdx.y * TY + ly - 1, gy = blockIdx.x * TX + lx - 1;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (hs.sm[k] < 0) continue;
       float val = 0.f;
-      if (pf && gx >= 0 && gx < h && gy >= 0 && gy < w) {
-        const long long o = (long long)gx * w + gy;
-        const float a = __ldg(pf + o);
-        const float b = __ldg(pp + o);
+      if (pf && hs.off[k] >= 0) {
+        const float a = __ldg(pf + hs.off[k]);
+        const float b = __ldg(pp + hs.off[k]);
         val = fmaf(c, a - b, a);
       }
-      ys[s][ly][lx] = val;
+      ysf[s * HALO_ELEMS + hs.sm[k]] = val;
     }
   };
 
-  // in-plane validity of the 8 neighbours (dy, dx) of this voxel
-  const bool okm_x = ix > 0, okp_x = ix + 1 < h, okm_y = iy > 0, okp_y = iy + 1 < w;
+  const float glam = lam * pc.inv_sp;
   double gsq = 0.0;
   if (THREE_D) {
     load_plane(-1, 2);
@@ -144,35 +215,34 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
     __syncthreads();
     if (inside) {
       const float yv = ys[s0][ty + 1][tx + 1];
-      float acc = 0.f;
-      // in-plane neighbours (dz = 0)
+      float2 acc = mk(0.f, 0.f);
+      // in-plane: 8 neighbours as 4 pairs
+      float nb[8], wv[8];
+      {
+        int q = 0;
 #pragma unroll
-      for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-        for (int dx = -1; dx <= 1; ++dx) {
-          if (dy == 0 && dx == 0) continue;
-          const bool ok = (dy < 0 ? okm_x : dy > 0 ? okp_x : true) &&
-                          (dx < 0 ? okm_y : dx > 0 ? okp_y : true);
-          const int k = (dy != 0) + (dx != 0);
-          const float wgt = THREE_D ? pc.w[k] : pc.w[k];
-          if (ok) acc = fmaf(wgt, rho_prime<P2>(yv - ys[s0][ty + 1 + dy][tx + 1 + dx], pc), acc);
+        for (int j = 0; j < 9; ++j) {
+          if (j == 4) continue;
+          nb[q] = ys[s0][ty + j / 3][tx + j % 3];
+          wv[q] = ipw.w8[j];
+          ++q;
         }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 g = drho2<P2>(mk(yv - nb[2 * i], yv - nb[2 * i + 1]), pc);
+        acc = pfma(mk(wv[2 * i], wv[2 * i + 1]), g, acc);
+      }
       if (THREE_D) {
-        const bool okz[2] = {z > 0 || FP.lo != nullptr, z + 1 < nz || FP.hi != nullptr};
+        // planes z-1 and z+1: same (dy, dx) paired across the two planes
+        const float lo_ok = (z > 0 || FP.lo != nullptr) ? 1.f : 0.f;
+        const float hi_ok = (z + 1 < nz || FP.hi != nullptr) ? 1.f : 0.f;
 #pragma unroll
-        for (int side = 0; side < 2; ++side) {
-          if (!okz[side]) continue;
-          const int sl = side ? sp : sm;
-#pragma unroll
-          for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) {
-              const bool ok = (dy < 0 ? okm_x : dy > 0 ? okp_x : true) &&
-                              (dx < 0 ? okm_y : dx > 0 ? okp_y : true);
-              const int k = 1 + (dy != 0) + (dx != 0);
-              if (ok)
-                acc = fmaf(pc.w[k], rho_prime<P2>(yv - ys[sl][ty + 1 + dy][tx + 1 + dx], pc), acc);
-            }
+        for (int j = 0; j < 9; ++j) {
+          const float a = ys[sm][ty + j / 3][tx + j % 3];
+          const float b = ys[sp][ty + j / 3][tx + j % 3];
+          const float2 g = drho2<P2>(mk(yv - a, yv - b), pc);
+          acc = pfma(mk(ipw.wz[j] * lo_ok, ipw.wz[j] * hi_ok), g, acc);
         }
       }
       const long long o = z * nn + (long long)ix * w + iy;
@@ -181,7 +251,7 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
         const float kfv = __ldg(Kf + o), kpv = __ldg(Kfp + o);
         ky = fmaf(c, kfv - kpv, kfv);
       }
-      const float grad = fmaf(lam, acc, ky - (rstar ? __ldg(rstar + o) : 0.f));
+      const float grad = fmaf(glam, acc.x + acc.y, ky - (rstar ? __ldg(rstar + o) : 0.f));
       if (write_grad) {
         f_new[o] = grad;
       } else {
@@ -189,7 +259,7 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
         if (NONNEG) fn = fmaxf(fn, 0.f);
         f_new[o] = fn;
       }
-      gsq += (double)grad * (double)grad;
+      gsq = fma((double)grad, (double)grad, gsq);
     }
     __syncthreads();
   }
@@ -205,24 +275,26 @@ __global__ void __launch_bounds__(TX* TY)
 k_energy_fid(Planes FN, const float* __restrict__ f, const float* __restrict__ Kfn,
              const float* __restrict__ Kf, const float* __restrict__ rstar,
              double* __restrict__ partial, int nz, int h, int w, int with_prior, PriorConsts pc) {
-  __shared__ float xs[2][TY + 2][TX + 2];
+  __shared__ float xs[2][HY][HX];
   __shared__ double red[TX * TY / 32];
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int iy = blockIdx.x * TX + tx;
   const int ix = blockIdx.y * TY + ty;
   const long long nn = (long long)h * w;
   const bool inside = ix < h && iy < w;
+  HaloSlots hs;
+  hs.init(h, w);
+  InPlaneW ipw;
+  ipw.init(ix, iy, h, w, pc);
+  float* xsf = &xs[0][0][0];
   auto load_plane = [&](int zz, int s) {
     const float* pf = FN.at(zz, nz, nn);
-    for (int e = threadIdx.x; e < (TY + 2) * (TX + 2); e += TX * TY) {
-      const int ly = e / (TX + 2), lx = e - ly * (TX + 2);
-      const int gx = blockIdx.y * TY + ly - 1, gy = blockIdx.x * TX + lx - 1;
-      float val = 0.f;
-      if (pf && gx >= 0 && gx < h && gy >= 0 && gy < w) val = __ldg(pf + (long long)gx * w + gy);
-      xs[s][ly][lx] = val;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (hs.sm[k] < 0) continue;
+      xsf[s * HALO_ELEMS + hs.sm[k]] = (pf && hs.off[k] >= 0) ? __ldg(pf + hs.off[k]) : 0.f;
     }
   };
-  const bool okp_x = ix + 1 < h, okm_y = iy > 0, okp_y = iy + 1 < w, okm_x = ix > 0;
   double e_acc = 0.0, fid = 0.0, dfid = 0.0;
   if (with_prior && THREE_D) load_plane(0, 0);
   for (int z = 0; z < nz; ++z) {
@@ -235,33 +307,32 @@ k_energy_fid(Planes FN, const float* __restrict__ f, const float* __restrict__ K
       const long long o = z * nn + (long long)ix * w + iy;
       const float fnv = __ldg(FN.main + o);
       const float kfn = Kfn ? __ldg(Kfn + o) : 0.f, rs = rstar ? __ldg(rstar + o) : 0.f;
-      if (Kfn) fid += (double)fnv * (double)fmaf(0.5f, kfn, -rs);
+      if (Kfn) fid = fma((double)fnv, (double)fmaf(0.5f, kfn, -rs), fid);
       if (f && Kfn) {
         const float fv = __ldg(f + o), kf = __ldg(Kf + o);
-        dfid += (double)(fnv - fv) * (double)(fmaf(0.5f, kfn + kf, 0.f) - rs);
+        dfid = fma((double)(fnv - fv), (double)(fmaf(0.5f, kfn + kf, 0.f) - rs), dfid);
       }
       if (with_prior) {
         const float xv = xs[s0][ty + 1][tx + 1];
-        float acc = 0.f;
-        // dz = 0: (0, 0, 1), (0, 1, -1), (0, 1, 0), (0, 1, 1)
-        if (okp_y) acc = fmaf(pc.w[1], rho<P2>(xv - xs[s0][ty + 1][tx + 2], pc), acc);
-        if (okp_x) {
-          if (okm_y) acc = fmaf(pc.w[2], rho<P2>(xv - xs[s0][ty + 2][tx], pc), acc);
-          acc = fmaf(pc.w[1], rho<P2>(xv - xs[s0][ty + 2][tx + 1], pc), acc);
-          if (okp_y) acc = fmaf(pc.w[2], rho<P2>(xv - xs[s0][ty + 2][tx + 2], pc), acc);
+        // half stencil in the plane: (0,0,1), (0,1,-1), (0,1,0), (0,1,1) as two pairs
+        float2 acc = mk(0.f, 0.f);
+        {
+          const float2 g0 = rho2<P2>(mk(xv - xs[s0][ty + 1][tx + 2], xv - xs[s0][ty + 2][tx]), pc);
+          acc = pfma(mk(ipw.w8[5], ipw.w8[6]), g0, acc);
+          const float2 g1 =
+              rho2<P2>(mk(xv - xs[s0][ty + 2][tx + 1], xv - xs[s0][ty + 2][tx + 2]), pc);
+          acc = pfma(mk(ipw.w8[7], ipw.w8[8]), g1, acc);
         }
-        if (up) {  // dz = 1: all nine (dy, dx)
+        if (up) {  // dz = 1: all nine (dy, dx): four pairs and one single (paired with a dummy)
 #pragma unroll
-          for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) {
-              const bool ok = (dy < 0 ? okm_x : dy > 0 ? okp_x : true) &&
-                              (dx < 0 ? okm_y : dx > 0 ? okp_y : true);
-              const int k = 1 + (dy != 0) + (dx != 0);
-              if (ok) acc = fmaf(pc.w[k], rho<P2>(xv - xs[s1][ty + 1 + dy][tx + 1 + dx], pc), acc);
-            }
+          for (int i = 0; i < 5; ++i) {
+            const int j0 = 2 * i, j1 = 2 * i + 1 < 9 ? 2 * i + 1 : 8;
+            const float2 g = rho2<P2>(mk(xv - xs[s1][ty + j0 / 3][tx + j0 % 3],
+                                         xv - xs[s1][ty + j1 / 3][tx + j1 % 3]), pc);
+            acc = pfma(mk(ipw.wz[j0], 2 * i + 1 < 9 ? ipw.wz[j1] : 0.f), g, acc);
+          }
         }
-        e_acc += (double)acc;
+        e_acc += (double)((acc.x + acc.y) * pc.inv_psp);
       }
     }
     __syncthreads();
@@ -295,10 +366,11 @@ static PriorConsts make_consts(double sigma, double p, double q, double T, const
   const double sp = pow(sigma, p);
   pc.inv_sp = (float)(1.0 / sp);
   pc.inv_psp = (float)(1.0 / (p * sp));
-  pc.log2_ts = (float)log2(T * sigma);
+  pc.c0 = (float)((p - q) * log2(T * sigma));
   pc.pq = (float)(p - q);
   pc.qp = (float)(q / p);
   pc.p = (float)p;
+  pc.pm1 = (float)(p - 1.0);
   pc.w[0] = 0.f;
   pc.w[1] = (float)w3[0];
   pc.w[2] = (float)w3[1];

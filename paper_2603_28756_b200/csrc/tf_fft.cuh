@@ -27,8 +27,9 @@ constexpr int TW_MAX = 16384;  // largest supported transform length
 // Concatenated per-length tables: W_L^j = e^{-2 pi i j/L} at word (L - 2) + j for
 // L = 2, 4, ..., TW_MAX, so the twiddles of one pass are contiguous in k.
 constexpr int TW_WORDS = 2 * TW_MAX - 2;
-// defined once: the library is a single translation unit (lib.cu)
-__device__ c32 g_twiddle[TW_WORDS];
+// one copy per translation unit (internal linkage, no relocatable device code);
+// every TU that runs FFTs fills its copy from ensure_init() via init_twiddles_tu()
+static __device__ c32 g_twiddle[TW_WORDS];
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 __host__ __device__ constexpr int pad_idx(int i) { return i + (i >> 4); }
@@ -311,6 +312,29 @@ template <int M, int E>
 __device__ __forceinline__ void store_canonical(const c32 (&v)[E], c32* sm, int t) {
 #pragma unroll
   for (int m = 0; m < E; ++m) sm[canon_word<M, E>(t, m)] = v[m];
+}
+
+// per-length tables W_L^j at word (L - 2) + j, computed in fp64
+static __global__ void k_twiddle_init(c32* tw) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= TW_WORDS) return;
+  int L = 2;
+  while (w >= 2 * L - 2) L <<= 1;  // table L occupies words [L-2, 2L-2)
+  const int j = w - (L - 2);
+  double s, c;
+  sincospi(-2.0 * (double)j / L, &s, &c);
+  tw[w] = mk((float)c, (float)s);
+}
+
+// fill this translation unit's table on the current device (synchronous)
+static inline cudaError_t init_twiddles_tu() {
+  c32* p = nullptr;
+  cudaError_t e = cudaGetSymbolAddress((void**)&p, g_twiddle);
+  if (e != cudaSuccess) return e;
+  k_twiddle_init<<<(TW_WORDS + 255) / 256, 256>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cudaDeviceSynchronize();
 }
 
 }  // namespace tf

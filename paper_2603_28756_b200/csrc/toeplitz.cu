@@ -536,19 +536,6 @@ __global__ void k_psf_finish(const c32* __restrict__ spec, c32* __restrict__ PQ,
   Bi[id] = (float)bim;
 }
 
-// per-length tables W_L^j at word (L - 2) + j (tf_fft.cuh), computed in fp64
-__global__ void k_twiddle_init(c32* tw) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= TW_WORDS) return;
-  int L = 2;
-  while (w >= 2 * L - 2) L <<= 1;  // table L occupies words [L-2, 2L-2)
-  const int j = w - (L - 2);
-  double s, c;
-  sincospi(-2.0 * (double)j / L, &s, &c);
-  tw[w] = mk((float)c, (float)s);
-}
-
-
 // ============================================================ host dispatch
 namespace {
 
@@ -835,12 +822,6 @@ int psf_build(int n, int M, const double* cs, int n_angles, int nd, void* PQ, fl
                            reinterpret_cast<char*>(ws), st);
 }
 
-int init_twiddles() {
-  c32* p = nullptr;
-  TF_TRY(check_cuda(cudaGetSymbolAddress((void**)&p, g_twiddle), "cudaGetSymbolAddress"));
-  k_twiddle_init<<<(TW_WORDS + 255) / 256, 256>>>(p);
-  TF_TRY(check_launch("k_twiddle_init"));
-  return check_cuda(cudaDeviceSynchronize(), "twiddle init sync");
-}
+int init_twiddles_toeplitz() { return check_cuda(init_twiddles_tu(), "twiddle init (toeplitz)"); }
 
 }  // namespace tf

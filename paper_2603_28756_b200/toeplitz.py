@@ -13,6 +13,7 @@ M >= 2N-1 and runs the fused real-FFT convolution of csrc/toeplitz.cu
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -36,6 +37,8 @@ __all__ = [
 
 # slices processed per apply pass; bounds the half-spectrum workspace
 _MAX_CHUNK_BYTES = 4 << 30
+# slices per K1 -> K2 -> K3 pass (0: as many as the workspace allows); tuning knob
+_CHUNK_SLICES = int(os.environ.get("TF_CHUNK_SLICES", "0"))
 
 
 def _is_7smooth(v: int) -> bool:
@@ -158,7 +161,7 @@ def apply_stack(psf: PsfKernel, x: torch.Tensor, out: torch.Tensor | None = None
     if aux is not None and (aux.shape != x.shape or not aux.is_contiguous()):
         raise ValueError("aux must match the input stack")
     per_slice = lib.tf_toeplitz_workspace_bytes(n, m, 1)
-    chunk = max(1, min(z, _MAX_CHUNK_BYTES // per_slice))
+    chunk = max(1, min(z, _MAX_CHUNK_BYTES // per_slice, _CHUNK_SLICES or z))
     ws = _device.workspace(per_slice * chunk)
     _lib.check(
         lib.tf_toeplitz_apply(x.data_ptr(), out.data_ptr(), _lib.ptr(aux), float(alpha),
