@@ -55,12 +55,11 @@ __host__ __device__ constexpr int nrb_of(int rows) { return (rows + RB - 1) / RB
 // Thread t owns k = t + T m (m < E/2); Z(M-k) sits in the upper half of partner
 // thread T-t and is exchanged through shared memory.  Stores are 32 B per k,
 // contiguous across the warp.  ZP: n_in <= M/2 (upper half of inputs is zero).
-template <int M, int E, int G, bool ZP>
+template <int M, int E, int G, bool ZP, int NB>
 __global__ void __launch_bounds__(G*(M / E), (M >= 8192 ? 1 : 2))
 k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
            long long x_slice_stride, long long x_row_stride) {
   constexpr int TT = M / E;
-  constexpr int NB = 2;
   constexpr int SB = group_stride(M, NB * G);
   constexpr int H = M / 2 + 1;
   constexpr int EL = ZP ? E / 2 : E;  // loaded elements
@@ -69,8 +68,11 @@ k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
   const int t = threadIdx.x - g * TT;
   const int z = blockIdx.y;
   const int nrb = nrb_of(rows);
-  const int rb = blockIdx.x * G + g;
-  const int r0 = rb * RB;
+  // NB == 2: a group owns a 4-row block; NB == 1: half a block (row pair b0)
+  const int unit = blockIdx.x * G + g;
+  const int rb = NB == 2 ? unit : unit >> 1;
+  const int b0 = NB == 2 ? 0 : (unit & 1);
+  const int r0 = rb * RB + 2 * b0;
   c32* sm = smem + g * NB * SB;
 
   const float* xr = x + z * x_slice_stride + (long long)r0 * x_row_stride;
@@ -99,14 +101,17 @@ k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
 
   float4* dst = reinterpret_cast<float4*>(T + ((long long)z * nrb + rb) * H * RB);
   auto emit = [&](int k, int m, bool self) {
+    float4 o[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const c32 zk = v[b][m];
       const c32 zm = self ? zk : sm[b * SB + M / 2 - k];
       const c32 xa = scale(mk(zk.x + zm.x, zk.y - zm.y), 0.5f);
       const c32 xb = scale(mk(zk.y + zm.y, zm.x - zk.x), 0.5f);
-      dst[2 * k + b] = make_float4(xa.x, xa.y, xb.x, xb.y);
+      o[b] = make_float4(xa.x, xa.y, xb.x, xb.y);
     }
+    if constexpr (NB == 2) st_global_v8(dst + 2 * k, o[0], o[NB - 1]);  // 32 B: all 4 rows
+    else dst[2 * k + b0] = o[0];
   };
 #pragma unroll
   for (int m = 0; m < E / 2; ++m) {
@@ -114,6 +119,98 @@ k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
     emit(k, m, k == 0);
   }
   if (t == 0) emit(M / 2, E / 2, true);
+}
+
+// Persistent K1 with a bulk-copied input stage.  Each CTA walks units u =
+// blockIdx.x + i * gridDim.x (unit = (slice, 4-row block)); the four input rows
+// of the next unit are fetched by the copy engine (cp.async.bulk, one 1-D copy
+// per row) into the single shared stage as soon as the current unit has read
+// it, so the load latency overlaps this unit's FFT.  Needs 16-byte aligned rows
+// of n_in * 4 bytes.  Same transform and output as k_rows_fwd (NB = 2).
+template <int M, int E, bool ZP>
+__global__ void __launch_bounds__(M / E, (M >= 8192 ? 1 : 2))
+k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
+              long long x_slice_stride, long long x_row_stride, long long nunits) {
+  constexpr int TT = M / E;
+  constexpr int NB = 2;
+  constexpr int SB = group_stride(M, NB);
+  constexpr int H = M / 2 + 1;
+  constexpr int EL = ZP ? E / 2 : E;
+  extern __shared__ __align__(128) c32 smem[];
+  c32* sm = smem;                                                   // exchange: NB * SB
+  float* stage = reinterpret_cast<float*>(smem + NB * SB);          // [RB][n_in]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + RB * n_in);  // 8-byte aligned
+  const int t = threadIdx.x;
+  const int nrb = nrb_of(rows);
+  const uint32_t row_bytes = (uint32_t)n_in * sizeof(float);
+  auto issue = [&](long long u) {
+    const int z = (int)(u / nrb), rb = (int)(u - (long long)z * nrb);
+    const int r0 = rb * RB;
+    const int nr = min(RB, rows - r0);
+    mbar_expect_tx(full, nr * row_bytes);
+    for (int q = 0; q < nr; ++q)
+      bulk_g2s(stage + q * n_in, x + z * x_slice_stride + (long long)(r0 + q) * x_row_stride,
+               row_bytes, full);
+  };
+  if (t == 0) {
+    mbar_init(full, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (t == 0 && (long long)blockIdx.x < nunits) issue(blockIdx.x);
+  int it = 0;
+  for (long long u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+    const int z = (int)(u / nrb), rb = (int)(u - (long long)z * nrb);
+    const int r0 = rb * RB;
+    mbar_wait(full, (uint32_t)(it & 1));
+    c32 v[NB][E];
+#pragma unroll
+    for (int m = 0; m < EL; ++m) {
+      const int j = t + TT * m;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        float a = 0.f, c = 0.f;
+        if (j < n_in) {
+          if (r0 + 2 * b < rows) a = stage[(2 * b) * n_in + j];
+          if (r0 + 2 * b + 1 < rows) c = stage[(2 * b + 1) * n_in + j];
+        }
+        v[b][m] = mk(a, c);
+      }
+    }
+    __syncthreads();  // the stage is free: refill it with the next unit
+    if (t == 0 && u + gridDim.x < nunits) {
+      fence_proxy_async_smem();
+      issue(u + gridDim.x);
+    }
+    fftn<M, E, false, ZP, false, NB>(v, sm, SB, t);
+#pragma unroll
+    for (int m = E / 2; m < E; ++m)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) sm[b * SB + t + TT * m - M / 2] = v[b][m];
+    __syncthreads();
+    float4* dst = reinterpret_cast<float4*>(T + ((long long)z * nrb + rb) * H * RB);
+    auto emit = [&](int k, int m, bool self) {
+      float4 o[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const c32 zk = v[b][m];
+        const c32 zm = self ? zk : sm[b * SB + M / 2 - k];
+        const c32 xa = scale(mk(zk.x + zm.x, zk.y - zm.y), 0.5f);
+        const c32 xb = scale(mk(zk.y + zm.y, zm.x - zk.x), 0.5f);
+        o[b] = make_float4(xa.x, xa.y, xb.x, xb.y);
+      }
+      st_global_v8(dst + 2 * k, o[0], o[1]);
+    };
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+      const int k = t + TT * m;
+      emit(k, m, k == 0);
+    }
+    if (t == 0) emit(M / 2, E / 2, true);
+    // the next unit's pass-0 exchange store must not overtake the mirror reads:
+    // its first shared write follows the stage barrier above, which every
+    // thread reaches only after finishing this unit
+  }
 }
 
 // ============================================================ K3: rows, inverse
@@ -125,30 +222,34 @@ k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
 // (m < E/2); the mirrored half comes from partner thread T-t via shared memory.
 // AUXBULK: the four aux rows are prefetched into shared memory by 1-D bulk
 // copies issued at kernel start (needs 16-byte aligned rows of n_out*4 bytes).
-template <int M, int E, int G, bool AUXBULK>
+template <int M, int E, int G, bool AUXBULK, int NB>
 __global__ void __launch_bounds__(G*(M / E), (M >= 8192 ? 1 : 2))
 k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __restrict__ aux,
            int rows, int n_out, long long o_slice_stride, long long o_row_stride, float alpha,
            float beta) {
   constexpr int TT = M / E;
-  constexpr int NB = 2;
   constexpr int H = M / 2 + 1;
   constexpr int SB = group_stride(M, NB * G);
+  constexpr int NR = 2 * NB;  // rows per group
   static_assert(2 * H <= SB, "pair buffer must fit the exchange buffer");
   extern __shared__ __align__(16) c32 smem[];
   const int g = threadIdx.x / TT;
   const int t = threadIdx.x - g * TT;
   const int z = blockIdx.y;
   const int nrb = nrb_of(rows);
-  const int rb = min(blockIdx.x * G + g, nrb - 1);  // surplus groups redo the last block
-  const bool writer = (int)(blockIdx.x * G + g) < nrb;
-  const int r0 = rb * RB;
+  // NB == 2: a group owns a 4-row block; NB == 1: half a block (row pair b0)
+  const int unit = blockIdx.x * G + g;
+  const int rb_raw = NB == 2 ? unit : unit >> 1;
+  const int b0 = NB == 2 ? 0 : (unit & 1);
+  const int rb = min(rb_raw, nrb - 1);  // surplus groups redo the last block
+  const bool writer = rb_raw < nrb;
+  const int r0 = rb * RB + 2 * b0;
   const float4* src = reinterpret_cast<const float4*>(T + ((long long)z * nrb + rb) * H * RB);
   c32* sm = smem + g * NB * SB;  // transform b: (Ya, Yb)(k) at words b*SB + 2k, +1
-  // AUXBULK region after the exchange buffers: [G][4][M/2] fp32 + one mbarrier
-  float* auxs = reinterpret_cast<float*>(smem + G * NB * SB) + g * RB * (M / 2);
+  // AUXBULK region after the exchange buffers: [G][NR][M/2] fp32 + one mbarrier
+  float* auxs = reinterpret_cast<float*>(smem + G * NB * SB) + g * NR * (M / 2);
   uint64_t* abar = reinterpret_cast<uint64_t*>(reinterpret_cast<float*>(smem + G * NB * SB) +
-                                               G * RB * (M / 2));
+                                               G * NR * (M / 2));
   const long long zo = z * o_slice_stride;
   if constexpr (AUXBULK) {
     if (threadIdx.x == 0) {
@@ -157,7 +258,7 @@ k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __re
     }
     __syncthreads();
     if (t == 0 && writer) {
-      const int nr = min(RB, rows - r0);
+      const int nr = min(NR, rows - r0);
       const uint32_t bytes = (uint32_t)n_out * sizeof(float);
       mbar_expect_tx(abar, nr * bytes);  // one arrival per group
       for (int q = 0; q < nr; ++q)
@@ -172,13 +273,14 @@ k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __re
   };
   float4 lo[E / 2][NB];
 #pragma unroll
-  for (int m = 0; m < E / 2; ++m)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) lo[m][b] = __ldg(src + 2 * (t + TT * m) + b);
+  for (int m = 0; m < E / 2; ++m) {
+    if constexpr (NB == 2) ld_global_nc_v8(src + 2 * (t + TT * m), lo[m][0], lo[m][NB - 1]);
+    else lo[m][0] = __ldg(src + 2 * (t + TT * m) + b0);
+  }
   float4 nyq[NB];
   if (t == 0)
 #pragma unroll
-    for (int b = 0; b < NB; ++b) nyq[b] = __ldg(src + 2 * (M / 2) + b);
+    for (int b = 0; b < NB; ++b) nyq[b] = __ldg(src + 2 * (M / 2) + b + b0);
 #pragma unroll
   for (int m = 0; m < E / 2; ++m)
 #pragma unroll
@@ -213,7 +315,7 @@ k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __re
   if (!writer) return;
 
 #pragma unroll
-  for (int q = 0; q < RB; ++q) {
+  for (int q = 0; q < NR; ++q) {
     const int r = r0 + q;
     if (r >= rows) break;
     float* o = out + zo + (long long)r * o_row_stride;
@@ -544,11 +646,16 @@ constexpr int E_DEFAULT = 16;
 template <int M>
 constexpr int eper() { return M < E_DEFAULT ? M : E_DEFAULT; }
 
-template <int M>
-constexpr int rows_g() {  // thread groups per CTA in K1/K3 (each group: one 4-row block)
+template <int M, int NB = 2>
+constexpr int rows_g() {  // thread groups per CTA in K1/K3 (each group: NB row pairs)
   constexpr int T = M / eper<M>();
-  constexpr int g = 256 / T;
+  constexpr int g = (NB == 2 ? 256 : 512) / T;
   return g < 1 ? 1 : (g > 16 ? 16 : g);
+}
+// row pairs per group in K1/K3: tuning knob TF_ROWS_NB (1 or 2; default 2)
+inline int rows_nb() {
+  static const int nb = getenv("TF_ROWS_NB") ? atoi(getenv("TF_ROWS_NB")) : 2;
+  return nb == 1 ? 1 : 2;
 }
 template <int M>
 constexpr int cols_g() {  // columns per CTA in the generic K2
@@ -567,19 +674,20 @@ int prep_kernel(K kern, size_t smem) {
   return TF_OK;
 }
 
-template <int M>
-int launch_rows_fwd(const float* x, c32* T, int rows, int n_in, long long xs, long long xr,
-                    long long nslices, cudaStream_t st) {
-  constexpr int E = eper<M>(), G = rows_g<M>();
+template <int M, int NB>
+int launch_rows_fwd_t(const float* x, c32* T, int rows, int n_in, long long xs, long long xr,
+                      long long nslices, cudaStream_t st) {
+  constexpr int E = eper<M>(), G = rows_g<M, NB>();
   constexpr int TT = M / E;
-  const size_t smem = sizeof(c32) * 2 * G * group_stride(M, 2 * G);
-  const int gx = (nrb_of(rows) + G - 1) / G;
+  const size_t smem = sizeof(c32) * NB * G * group_stride(M, NB * G);
+  const int units = nrb_of(rows) * (2 / NB);
+  const int gx = (units + G - 1) / G;
   KernelTimer tm;
   timer_begin(tm, 0, st);
   for (long long z0 = 0; z0 < nslices; z0 += 65535) {
     const int nz = (int)std::min<long long>(65535, nslices - z0);
     c32* Tz = T + z0 * (long long)(M / 2 + 1) * RB * nrb_of(rows);
-    auto kern = (2 * n_in <= M) ? k_rows_fwd<M, E, G, true> : k_rows_fwd<M, E, G, false>;
+    auto kern = (2 * n_in <= M) ? k_rows_fwd<M, E, G, true, NB> : k_rows_fwd<M, E, G, false, NB>;
     TF_TRY(prep_kernel(kern, smem));
     kern<<<dim3(gx, nz), G * TT, smem, st>>>(x + z0 * xs, Tz, rows, n_in, xs, xr);
   }
@@ -588,20 +696,60 @@ int launch_rows_fwd(const float* x, c32* T, int rows, int n_in, long long xs, lo
 }
 
 template <int M>
-int launch_rows_inv(const c32* T, float* out, const float* aux, int rows, int n_out,
-                    long long os, long long orow, float alpha, float beta, long long nslices,
-                    cudaStream_t st) {
-  constexpr int E = eper<M>(), G = rows_g<M>();
+int launch_rows_fwd_pf(const float* x, c32* T, int rows, int n_in, long long xs, long long xr,
+                       long long nslices, cudaStream_t st) {
+  constexpr int E = eper<M>();
+  constexpr int TT = M / E;
+  const size_t smem = sizeof(c32) * 2 * group_stride(M, 2) + sizeof(float) * RB * n_in + 16;
+  auto kern = (2 * n_in <= M) ? k_rows_fwd_pf<M, E, true> : k_rows_fwd_pf<M, E, false>;
+  TF_TRY(prep_kernel(kern, smem));
+  int per_sm = 0;
+  TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, smem),
+                    "occupancy"));
+  const long long nunits = (long long)nrb_of(rows) * nslices;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(nunits,
+                                                                  (long long)std::max(1, per_sm) * num_sms()));
+  KernelTimer tm;
+  timer_begin(tm, 0, st);
+  kern<<<grid, TT, smem, st>>>(x, T, rows, n_in, xs, xr, nunits);
+  timer_end(tm);
+  return check_launch("k_rows_fwd_pf");
+}
+
+// input prefetch variant: TF_ROWS_PF (default 1) when rows are 16-byte aligned blocks
+inline bool rows_pf() {
+  static const int pf = getenv("TF_ROWS_PF") ? atoi(getenv("TF_ROWS_PF")) : 1;
+  return pf != 0;
+}
+
+template <int M>
+int launch_rows_fwd(const float* x, c32* T, int rows, int n_in, long long xs, long long xr,
+                    long long nslices, cudaStream_t st) {
+  const size_t pf_smem = sizeof(c32) * 2 * group_stride(M, 2) + sizeof(float) * RB * n_in + 16;
+  if (M >= 1024 && rows_pf() && n_in % 4 == 0 && xr % 4 == 0 && xs % 4 == 0 &&
+      reinterpret_cast<uintptr_t>(x) % 16 == 0 && pf_smem <= 200 * 1024)
+    return launch_rows_fwd_pf<M>(x, T, rows, n_in, xs, xr, nslices, st);
+  if (M >= 1024 && rows_nb() == 1)
+    return launch_rows_fwd_t<M, 1>(x, T, rows, n_in, xs, xr, nslices, st);
+  return launch_rows_fwd_t<M, 2>(x, T, rows, n_in, xs, xr, nslices, st);
+}
+
+template <int M, int NB>
+int launch_rows_inv_t(const c32* T, float* out, const float* aux, int rows, int n_out,
+                      long long os, long long orow, float alpha, float beta, long long nslices,
+                      cudaStream_t st) {
+  constexpr int E = eper<M>(), G = rows_g<M, NB>();
   constexpr int TT = M / E;
   if (2 * n_out > M) return fail_arg("k_rows_inv: n_out %d exceeds M/2", n_out);
   // bulk-prefetch aux rows when they are 16-byte aligned blocks
   const bool bulk = aux && (n_out % 4 == 0) && (orow % 4 == 0) && (os % 4 == 0) &&
                     (reinterpret_cast<uintptr_t>(aux) % 16 == 0);
-  const size_t smem = sizeof(c32) * 2 * G * group_stride(M, 2 * G) +
-                      (bulk ? sizeof(float) * G * RB * (M / 2) + 16 : 0);
-  auto kern = bulk ? k_rows_inv<M, E, G, true> : k_rows_inv<M, E, G, false>;
+  const size_t smem = sizeof(c32) * NB * G * group_stride(M, NB * G) +
+                      (bulk ? sizeof(float) * G * 2 * NB * (M / 2) + 16 : 0);
+  auto kern = bulk ? k_rows_inv<M, E, G, true, NB> : k_rows_inv<M, E, G, false, NB>;
   TF_TRY(prep_kernel(kern, smem));
-  const int gx = (nrb_of(rows) + G - 1) / G;
+  const int units = nrb_of(rows) * (2 / NB);
+  const int gx = (units + G - 1) / G;
   KernelTimer tm;
   timer_begin(tm, 2, st);
   for (long long z0 = 0; z0 < nslices; z0 += 65535) {
@@ -612,6 +760,15 @@ int launch_rows_inv(const c32* T, float* out, const float* aux, int rows, int n_
   }
   timer_end(tm);
   return check_launch("k_rows_inv");
+}
+
+template <int M>
+int launch_rows_inv(const c32* T, float* out, const float* aux, int rows, int n_out,
+                    long long os, long long orow, float alpha, float beta, long long nslices,
+                    cudaStream_t st) {
+  if (M >= 1024 && rows_nb() == 1)
+    return launch_rows_inv_t<M, 1>(T, out, aux, rows, n_out, os, orow, alpha, beta, nslices, st);
+  return launch_rows_inv_t<M, 2>(T, out, aux, rows, n_out, os, orow, alpha, beta, nslices, st);
 }
 
 // 4-D tensor map over the row-blocked half spectrum: dims (fp32 units)
