@@ -16,7 +16,7 @@ from pathlib import Path
 import torch
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libtomoforge_b200.so"
+LIB_PATH = Path(os.environ.get("TF_LIB_PATH", _HERE / "libtomoforge_b200.so"))
 
 _c_void_p = ctypes.c_void_p
 _c_int = ctypes.c_int

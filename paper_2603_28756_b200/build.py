@@ -15,8 +15,11 @@ from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
-LIB = HERE / "libtomoforge_b200.so"
-OBJ = HERE.parent / "build" / "obj"
+# tuning builds: TF_BUILD_DEFINES="-DTF_TW_MODE=2" TF_BUILD_OUT=/path/lib.so (separate objects)
+_DEFINES = os.environ.get("TF_BUILD_DEFINES", "").split()
+LIB = Path(os.environ.get("TF_BUILD_OUT", HERE / "libtomoforge_b200.so"))
+OBJ = HERE.parent / "build" / ("obj" + "".join(d.replace("-D", "_").replace("=", "")
+                                               for d in _DEFINES))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -45,7 +48,7 @@ def _compile(nvcc: str, src: Path, verbose: bool):
     newest_dep = max(p.stat().st_mtime for p in [src] + headers() + [Path(__file__)])
     if obj.exists() and obj.stat().st_mtime >= newest_dep:
         return obj, None
-    cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc, *NVCC_FLAGS, *_DEFINES, "-c", str(src), "-o", str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)

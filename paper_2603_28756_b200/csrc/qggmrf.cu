@@ -185,33 +185,63 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
   ipw.init(ix, iy, h, w, pc);
   float* ysf = &ys[0][0][0];
 
-  // y on plane zz into ring slot s (0 outside the grid or on an invalid plane)
-  auto load_plane = [&](int zz, int s) {
+  // Software pipeline: the halo-tile values of the next plane (raw f and
+  // f_prev at this thread's two slots) and the per-voxel operands (K f, K f_prev,
+  // R*g) of the next plane are loaded into registers one step ahead, so global
+  // latency overlaps the current plane's stencil.
+  float hf[2], hp[2];
+  auto fetch_plane = [&](int zz) {
     const float* pf = F.at(zz, nz, nn);
     const float* pp = FP.at(zz, nz, nn);
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      if (hs.sm[k] < 0) continue;
-      float val = 0.f;
-      if (pf && hs.off[k] >= 0) {
-        const float a = __ldg(pf + hs.off[k]);
-        const float b = __ldg(pp + hs.off[k]);
-        val = fmaf(c, a - b, a);
+      hf[k] = hp[k] = 0.f;
+      if (hs.sm[k] >= 0 && pf && hs.off[k] >= 0) {
+        hf[k] = __ldg(pf + hs.off[k]);
+        hp[k] = __ldg(pp + hs.off[k]);
       }
-      ysf[s * HALO_ELEMS + hs.sm[k]] = val;
     }
+  };
+  // y = f + c (f - f_prev) into ring slot s (0 outside the grid / invalid plane)
+  auto commit_plane = [&](int s) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (hs.sm[k] >= 0) ysf[s * HALO_ELEMS + hs.sm[k]] = fmaf(c, hf[k] - hp[k], hf[k]);
+  };
+  float nkf = 0.f, nkp = 0.f, nrs = 0.f;
+  auto fetch_ops = [&](int zz) {
+    if (!inside || zz >= nz) return;
+    const long long o = zz * nn + (long long)ix * w + iy;
+    if (Kf) {
+      nkf = __ldg(Kf + o);
+      nkp = __ldg(Kfp + o);
+    }
+    if (rstar) nrs = __ldg(rstar + o);
   };
 
   const float glam = lam * pc.inv_sp;
   double gsq = 0.0;
   if (THREE_D) {
-    load_plane(-1, 2);
-    load_plane(0, 0);
+    fetch_plane(-1);
+    commit_plane(2);
+    fetch_plane(0);
+    commit_plane(0);
+    fetch_plane(1);
+  } else {
+    fetch_plane(0);
   }
+  fetch_ops(0);
   for (int z = 0; z < nz; ++z) {
     const int s0 = THREE_D ? z % 3 : 0, sp = (z + 1) % 3, sm = (z + 2) % 3;  // z, z+1, z-1
-    if (THREE_D) load_plane(z + 1, sp);
-    else load_plane(z, 0);  // 8-neighbour stencil: slices are independent
+    if (THREE_D) {
+      commit_plane(sp);      // plane z+1, loaded during the previous step
+      fetch_plane(z + 2);    // in flight during this step
+    } else {
+      commit_plane(0);       // 8-neighbour stencil: slices are independent
+      if (z + 1 < nz) fetch_plane(z + 1);
+    }
+    const float kfv = nkf, kpv = nkp, rsv = nrs;
+    fetch_ops(z + 1);
     __syncthreads();
     if (inside) {
       const float yv = ys[s0][ty + 1][tx + 1];
@@ -246,12 +276,8 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
         }
       }
       const long long o = z * nn + (long long)ix * w + iy;
-      float ky = 0.f;
-      if (Kf) {
-        const float kfv = __ldg(Kf + o), kpv = __ldg(Kfp + o);
-        ky = fmaf(c, kfv - kpv, kfv);
-      }
-      const float grad = fmaf(glam, acc.x + acc.y, ky - (rstar ? __ldg(rstar + o) : 0.f));
+      const float ky = fmaf(c, kfv - kpv, kfv);
+      const float grad = fmaf(glam, acc.x + acc.y, ky - rsv);
       if (write_grad) {
         f_new[o] = grad;
       } else {
@@ -287,33 +313,65 @@ k_energy_fid(Planes FN, const float* __restrict__ f, const float* __restrict__ K
   InPlaneW ipw;
   ipw.init(ix, iy, h, w, pc);
   float* xsf = &xs[0][0][0];
-  auto load_plane = [&](int zz, int s) {
+  // software pipeline as in K4: next plane's halo values and per-voxel operands
+  // are fetched into registers one step ahead
+  float hv[2];
+  auto fetch_plane = [&](int zz) {
     const float* pf = FN.at(zz, nz, nn);
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      if (hs.sm[k] < 0) continue;
-      xsf[s * HALO_ELEMS + hs.sm[k]] = (pf && hs.off[k] >= 0) ? __ldg(pf + hs.off[k]) : 0.f;
+    for (int k = 0; k < 2; ++k)
+      hv[k] = (hs.sm[k] >= 0 && pf && hs.off[k] >= 0) ? __ldg(pf + hs.off[k]) : 0.f;
+  };
+  auto commit_plane = [&](int s) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (hs.sm[k] >= 0) xsf[s * HALO_ELEMS + hs.sm[k]] = hv[k];
+  };
+  float n_fn = 0.f, n_kfn = 0.f, n_rs = 0.f, n_f = 0.f, n_kf = 0.f;
+  auto fetch_ops = [&](int zz) {
+    if (!inside || zz >= nz) return;
+    const long long o = zz * nn + (long long)ix * w + iy;
+    if (!with_prior) n_fn = __ldg(FN.main + o);  // with the prior it is the tile centre
+    if (Kfn) n_kfn = __ldg(Kfn + o);
+    if (rstar) n_rs = __ldg(rstar + o);
+    if (f && Kfn) {
+      n_f = __ldg(f + o);
+      n_kf = __ldg(Kf + o);
     }
   };
   double e_acc = 0.0, fid = 0.0, dfid = 0.0;
-  if (with_prior && THREE_D) load_plane(0, 0);
+  if (with_prior) {
+    if (THREE_D) {
+      fetch_plane(0);
+      commit_plane(0);
+      fetch_plane(1);
+    } else {
+      fetch_plane(0);
+    }
+  }
+  fetch_ops(0);
   for (int z = 0; z < nz; ++z) {
     const int s0 = THREE_D ? (z & 1) : 0, s1 = (z + 1) & 1;
     const bool up = THREE_D && (z + 1 < nz || FN.hi != nullptr);
-    if (with_prior && up) load_plane(z + 1, s1);
-    if (with_prior && !THREE_D) load_plane(z, 0);
+    if (with_prior) {
+      if (THREE_D) {
+        commit_plane(s1);  // plane z+1 (zeros past an absent halo; unused then)
+        fetch_plane(z + 2);
+      } else {
+        commit_plane(0);
+        if (z + 1 < nz) fetch_plane(z + 1);
+      }
+    }
+    float fnv = n_fn;
+    const float kfn = n_kfn, rs = n_rs, fv = n_f, kf = n_kf;
+    fetch_ops(z + 1);
     __syncthreads();
     if (inside) {
-      const long long o = z * nn + (long long)ix * w + iy;
-      const float fnv = __ldg(FN.main + o);
-      const float kfn = Kfn ? __ldg(Kfn + o) : 0.f, rs = rstar ? __ldg(rstar + o) : 0.f;
+      if (with_prior) fnv = xs[s0][ty + 1][tx + 1];
       if (Kfn) fid = fma((double)fnv, (double)fmaf(0.5f, kfn, -rs), fid);
-      if (f && Kfn) {
-        const float fv = __ldg(f + o), kf = __ldg(Kf + o);
-        dfid = fma((double)(fnv - fv), (double)(fmaf(0.5f, kfn + kf, 0.f) - rs), dfid);
-      }
+      if (f && Kfn) dfid = fma((double)(fnv - fv), (double)(fmaf(0.5f, kfn + kf, 0.f) - rs), dfid);
       if (with_prior) {
-        const float xv = xs[s0][ty + 1][tx + 1];
+        const float xv = fnv;
         // half stencil in the plane: (0,0,1), (0,1,-1), (0,1,0), (0,1,1) as two pairs
         float2 acc = mk(0.f, 0.f);
         {

@@ -27,9 +27,16 @@ constexpr int TW_MAX = 16384;  // largest supported transform length
 // Concatenated per-length tables: W_L^j = e^{-2 pi i j/L} at word (L - 2) + j for
 // L = 2, 4, ..., TW_MAX, so the twiddles of one pass are contiguous in k.
 constexpr int TW_WORDS = 2 * TW_MAX - 2;
+// Direct power tables for radix-16 passes (TwDirect): for NS in {2,4,8,16}
+// the powers W_{16 NS}^{k r} laid out [r][k] at tws_base(NS); for the M = 4096
+// last pass (NS = 256, k = t) the powers W_4096^{t r} laid out [r-1][t].
+constexpr int TWS_WORDS = 16 * 31;
+__host__ __device__ constexpr int tws_base(int ns) { return 16 * (ns - 1); }
 // one copy per translation unit (internal linkage, no relocatable device code);
 // every TU that runs FFTs fills its copy from ensure_init() via init_twiddles_tu()
 static __device__ c32 g_twiddle[TW_WORDS];
+static __device__ c32 g_tw_small[TWS_WORDS];
+static __device__ c32 g_tw_t256[15 * 256];
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 __host__ __device__ constexpr int pad_idx(int i) { return i + (i >> 4); }
@@ -191,12 +198,34 @@ struct PassTw {
   static constexpr int NS = S::ns(P);
   static constexpr int ST = E / R;
   c32 w[ST][R];
+  // table entry W^k + log-depth product tree for the other powers (FP work)
   __device__ __forceinline__ void from_table(int t) {
 #pragma unroll
     for (int i = 0; i < ST; ++i) {
-      w[i][1] = tw_w<NS * R>((t + i * S::T) & (NS - 1));
+      const int k = (t + i * S::T) & (NS - 1);
+      w[i][1] = tw_w<NS * R>(k);
 #pragma unroll
       for (int r = 2; r < R; ++r) w[i][r] = cmul(w[i][r / 2], w[i][r - r / 2]);
+    }
+  }
+  // every power straight from a table where one exists (memory instead of FP
+  // work; used by the FMA-bound column kernel): [r][k] tables for NS <= 16 and
+  // the per-thread [r][t] table of the M = 4096 last pass
+  __device__ __forceinline__ void from_table_direct(int t) {
+#pragma unroll
+    for (int i = 0; i < ST; ++i) {
+      const int k = (t + i * S::T) & (NS - 1);
+      if constexpr (R == 16 && NS >= 2 && NS <= 16) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) w[i][r] = g_tw_small[tws_base(NS) + r * NS + k];
+      } else if constexpr (R == 16 && NS == 256 && S::T == 256) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) w[i][r] = __ldg(g_tw_t256 + (r - 1) * 256 + k);
+      } else {
+        w[i][1] = tw_w<NS * R>(k);
+#pragma unroll
+        for (int r = 2; r < R; ++r) w[i][r] = cmul(w[i][r / 2], w[i][r - r / 2]);
+      }
     }
   }
 };
@@ -206,6 +235,14 @@ struct TwTable {
   template <int M, int E, int P>
   __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
     tw.from_table(t);
+  }
+};
+
+// direct power tables (see PassTw::from_table_direct)
+struct TwDirect {
+  template <int M, int E, int P>
+  __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
+    tw.from_table_direct(t);
   }
 };
 
@@ -326,12 +363,33 @@ static __global__ void k_twiddle_init(c32* tw) {
   tw[w] = mk((float)c, (float)s);
 }
 
-// fill this translation unit's table on the current device (synchronous)
+static __global__ void k_twiddle_init_small(c32* small, c32* t256) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  double s, c;
+  if (w < TWS_WORDS) {
+    int ns = 1;
+    while (w >= tws_base(2 * ns)) ns *= 2;  // segment [tws_base(ns), tws_base(2 ns))
+    const int e = w - tws_base(ns), r = e / ns, k = e - r * ns;
+    const int L = 16 * ns;
+    sincospi(-2.0 * (double)((k * r) % L) / L, &s, &c);
+    small[w] = mk((float)c, (float)s);
+  }
+  if (w < 15 * 256) {
+    const int r = w / 256 + 1, t = w % 256;
+    sincospi(-2.0 * (double)((t * r) % 4096) / 4096.0, &s, &c);
+    t256[w] = mk((float)c, (float)s);
+  }
+}
+
+// fill this translation unit's tables on the current device (synchronous)
 static inline cudaError_t init_twiddles_tu() {
-  c32* p = nullptr;
+  c32 *p = nullptr, *q = nullptr, *u = nullptr;
   cudaError_t e = cudaGetSymbolAddress((void**)&p, g_twiddle);
+  if (e == cudaSuccess) e = cudaGetSymbolAddress((void**)&q, g_tw_small);
+  if (e == cudaSuccess) e = cudaGetSymbolAddress((void**)&u, g_tw_t256);
   if (e != cudaSuccess) return e;
   k_twiddle_init<<<(TW_WORDS + 255) / 256, 256>>>(p);
+  k_twiddle_init_small<<<(15 * 256 + 255) / 256, 256>>>(q, u);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return cudaDeviceSynchronize();

@@ -467,7 +467,7 @@ k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict_
   PassTw<M, E, FftShape<M, E>::NP - 1> last_tw;
   if constexpr (CACHE) last_tw.from_table(t);
   const TwLastCached<M, E> twc{&last_tw};
-  const TwTable twt;
+  const TwDirect twt;
   c32 pq[E];
   float bi[FLIP ? E : 1];
   const int col_len = nrb * RB;
@@ -496,7 +496,7 @@ k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict_
     }
     mbar_arrive(&empty[s]);
     if constexpr (CACHE) fftn<M, E, false, true, false, NB, TwLastCached<M, E>, PP>(v, xbuf, SB, t, twc);
-    else fftn<M, E, false, true, false, NB, TwTable, PP>(v, xbuf, SB, t, twt);
+    else fftn<M, E, false, true, false, NB, TwDirect, PP>(v, xbuf, SB, t, twt);
     // refill stage s with item i + S once every thread has released it
     if (t == 0 && i + S < nitems) {
       mbar_wait(&empty[s], parity);
@@ -513,7 +513,7 @@ k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict_
         }
       }
     if constexpr (CACHE) fftn<M, E, true, false, true, NB, TwLastCached<M, E>, PP>(v, xbuf, SB, t, twc);
-    else fftn<M, E, true, false, true, NB, TwTable, PP>(v, xbuf, SB, t, twt);
+    else fftn<M, E, true, false, true, NB, TwDirect, PP>(v, xbuf, SB, t, twt);
     if constexpr (PP) {
       const int H = M / 2 + 1;
 #pragma unroll
@@ -803,10 +803,10 @@ int encode_tmap(CUtensorMap* map, c32* T, int M, int nrb, long long nslices, int
 
 constexpr int CONV_STAGES = 2;
 
-template <int M, bool FLIP, int NB, bool CACHE, bool PP = false>
+template <int M, bool FLIP, int NB, bool CACHE, bool PP = false, int EOVR = 0>
 int launch_cols_conv_tma_t(c32* T, const c32* PQ, const float* Bi, int col_len,
                            long long nslices, cudaStream_t st) {
-  constexpr int E = eper<M>();
+  constexpr int E = EOVR ? EOVR : eper<M>();
   constexpr int TT = M / E;
   const int ncols = M / 2 + 1;
   const int nrb = nrb_of(col_len);
@@ -856,7 +856,8 @@ int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long l
   // tuning/debug knob: TF_K2 = generic | nb1 | nb1c | nb2 | nb2c (default nb1)
   static const char* k2 = getenv("TF_K2");
   static const int variant = !k2 ? 0 : !strcmp(k2, "generic") ? -1 : !strcmp(k2, "nb1") ? 0
-                          : !strcmp(k2, "nb1c") ? 1 : !strcmp(k2, "nb2") ? 2 : !strcmp(k2, "nb1p") ? 4 : 3;
+                          : !strcmp(k2, "nb1c") ? 1 : !strcmp(k2, "nb2") ? 2 : !strcmp(k2, "nb1p") ? 4
+                          : !strcmp(k2, "e8") ? 5 : 3;
   if constexpr (M >= 1024 && M <= 4096) {
     switch (variant) {
       case 0: return flip ? launch_cols_conv_tma_t<M, true, 1, false>(T, PQ, Bi, col_len, nslices, st)
@@ -869,6 +870,8 @@ int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long l
                           : launch_cols_conv_tma_t<M, false, 2, true>(T, PQ, Bi, col_len, nslices, st);
       case 4: return flip ? launch_cols_conv_tma_t<M, true, 1, false, true>(T, PQ, Bi, col_len, nslices, st)
                           : launch_cols_conv_tma_t<M, false, 1, false, true>(T, PQ, Bi, col_len, nslices, st);
+      case 5: return flip ? launch_cols_conv_tma_t<M, true, 1, false, false, 8>(T, PQ, Bi, col_len, nslices, st)
+                          : launch_cols_conv_tma_t<M, false, 1, false, false, 8>(T, PQ, Bi, col_len, nslices, st);
       default: break;
     }
   }
