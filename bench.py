@@ -124,8 +124,14 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # TF_DIST_BACKEND=gloo runs the multi-rank path on a single GPU (testing only)
+        backend = os.environ.get("TF_DIST_BACKEND", "nccl")
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -144,7 +150,8 @@ def max_over_ranks(value: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -307,21 +314,10 @@ def run_ours(args, world, rank, local):
 
 
 def _make_context(tf, psf, geom, z, rank):
-    """FidelityContext for a synthetic randn sinogram (R*g on the GPU when available)."""
-    import torch
-
-    from paper_2603_28756_b200.toeplitz import FidelityContext
-
+    """FidelityContext of a synthetic randn sinogram: R*g by the GPU NUFFT (K7/K8)."""
     g = np.random.default_rng(2000 + rank).standard_normal((z, N_ANGLES, N_BINS))
-    try:
-        plan = tf.NufftPlan(N_SIDE, tf.polar_sampling(geom), 1e-6)
-        sino = tf.Sinogram(angles=geom.angles, data=g)
-        return tf.fidelity_context(plan, psf, sino)
-    except (AttributeError, ImportError):
-        # NUFFT back-projection not built yet: a synthetic R*g of the same shape
-        gen = torch.Generator(device="cuda").manual_seed(3000 + rank)
-        rs = torch.randn((z, N_SIDE, N_SIDE), generator=gen, device="cuda")
-        return FidelityContext(psf=psf, rstar=rs, g_norm_sq=float(np.sum(g ** 2)))
+    plan = tf.NufftPlan(N_SIDE, tf.polar_sampling(geom), 1e-6)
+    return tf.fidelity_context(plan, psf, tf.Sinogram(angles=geom.angles, data=g))
 
 
 def _e2e(tf, ctx, z, world, steps):
@@ -385,6 +381,9 @@ def _mbir(tf, args, world, rank):
     peak = _peak_hbm()["value"]
     del ctx, f0
     torch.cuda.empty_cache()
+    if world > 1:
+        return _mbir_distributed(tf, z, world, rank, prm, L, timed, {
+            "psf": t_psf, "rstar_nufft": t_rstar, "fbp_nufft": t_fbp}, per_it, bpv, peak)
     hier = tf.GridHierarchy(levels=(512, 1024, 2048), iters_per_level=(40, 20, 10))
     _, t_hier = timed(lambda: tf.solve_hierarchical(
         sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300, lipschitz=L), use_fbp_init=True))
@@ -397,6 +396,33 @@ def _mbir(tf, args, world, rank):
         "hierarchical_3level_ms": t_hier,
         "hierarchical_schedule": "levels (512, 1024, 2048), iterations (40, 20, 10), FBP init, "
                                  "Lanczos-3 upsampling, L fixed from the finest level",
+    }
+
+
+def _mbir_distributed(tf, z, world, rank, prm, L, timed, setup, per_it_local, bpv, peak):
+    """N > 1: the z-slab solver over NCCL (runtime.distributed_solve, one slab of
+    ``z`` slices per rank, halo exchange + 3-scalar allreduce every iteration)."""
+    from paper_2603_28756_b200.runtime import distributed_solve
+
+    g = np.random.default_rng(4100).standard_normal((z * world, N_ANGLES, N_BINS))
+    sino = tf.Sinogram(angles=angles(), data=g)
+    iters = 10
+    cfg = tf.SolverConfig(max_iters=iters, tol=1e-300, lipschitz=L)
+    distributed_solve(sino, N_SIDE, prm, tf.SolverConfig(max_iters=2, tol=1e-300, lipschitz=L),
+                      world, gather="none")  # warm (plans, PSF, NCCL channels)
+    (_, recs), t_total = timed(lambda: distributed_solve(sino, N_SIDE, prm, cfg, world,
+                                                         gather="none"))
+    step_ms = max_over_ranks(float(np.median([r.step_time for r in recs[1:]])) * 1e3, world)
+    return {
+        "workload": f"z-slab MBIR: {z * world} x 2048^2 over {world} GPUs ({z} slices per GPU), "
+                    "128 angles, Nd=2048, qGGMRF lam=5e-4",
+        "setup_ms_per_gpu": setup,
+        "solve_ms_per_iter_single_gpu_slab": per_it_local,
+        "distributed_ms_per_iter": step_ms,
+        "distributed_total_ms_incl_setup": t_total,
+        "solve_bytes_per_voxel_iter": bpv,
+        "solve_hbm_frac": bpv * z * N_SIDE * N_SIDE / (step_ms / 1e3) / 1e9 / peak,
+        "comm_per_iter": "2 halo planes of 16.8 MB per interior boundary + one 3 x fp64 allreduce",
     }
 
 

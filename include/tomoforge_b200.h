@@ -130,6 +130,14 @@ int tf_nufft_type1(const void* d_samples, long long sample_stride, long long nsl
                    const float* d_deapod, float scale, int out_complex, void* d_out, void* d_ws,
                    long long ws_bytes, void* stream);
 
+/* Plan tables of tf_nufft_type1 on the device: for every sample m (d_kxy:
+ * [S][2] fp64 radial-frequency coordinates) and axis, the first window index
+ * a0 = ceil(k os / (2 pi) - width/2) mod os (d_ab: int32 [S][2]) and the width
+ * Kaiser-Bessel weights I0(beta sqrt(1 - (2x/width)^2)) (d_wts: fp32 [S][2*width]),
+ * evaluated in fp64 (replaces NufftPlan._windows, nufft.py:158-164). */
+int tf_nufft_plan_weights(const double* d_kxy, long long n_samples, int os, int width,
+                          double beta, void* d_ab, float* d_wts, void* stream);
+
 /* ---- Lanczos-3 resampling (K9) ----------------------------------------------
  * One axis of the separable upsampler of multires.upsample (multires.py:145-195):
  *   d_out[o][t][i] = sum_{k < taps} d_weights[t][k] * d_in[o][d_start[t] + k][i]

@@ -106,9 +106,9 @@ def wrap_like(kind: str, t: torch.Tensor):
         return t[0]
     host = to_host64(t)
     if kind == "image":
-        return ImageGrid(host[0])
+        return ImageGrid._owned(host[0])
     if kind == "volume":
-        return Volume(host)
+        return Volume._owned(host)
     if kind == "array2":
         return host[0]
     return host

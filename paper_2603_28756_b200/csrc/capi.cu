@@ -116,6 +116,8 @@ int energy_fid(const float* fn, const float* fn_hi, const float* f, const float*
 int dot2(const float* x, const float* a, const float* b, long long n, double* out, double* ws,
          cudaStream_t st);
 size_t nufft_workspace_bytes(int os, long long nslices);
+int nufft_plan_weights(const double* kxy, long long S, int os, int w, double beta, void* ab,
+                       float* wts, cudaStream_t st);
 int resample_axis(const float* in, float* out, long long outer, int n_src, int n_tgt,
                   long long inner, const int* s0, const float* w, int K, cudaStream_t st);
 int detector_rows(const float* rows, long long nrows, int nd, int n_angles, const void* sph,
@@ -260,6 +262,14 @@ int tf_nufft_type1(const void* d_samples, long long sample_stride, long long nsl
   return nufft_type1(d_samples, sample_stride, nslices, n, os, width, d_tile_ptr, d_tile_idx, d_ab,
                      d_wts, d_prephase, d_deapod, scale, out_complex, d_out, d_ws,
                      (size_t)ws_bytes, (cudaStream_t)stream);
+}
+
+int tf_nufft_plan_weights(const double* d_kxy, long long n_samples, int os, int width,
+                          double beta, void* d_ab, float* d_wts, void* stream) {
+  TF_TRY(ensure_init());
+  if (n_samples < 0 || os < 2 || width < 2 || width > 16) return fail_arg("bad plan arguments");
+  if (n_samples > 0 && (!d_kxy || !d_ab || !d_wts)) return fail_arg("null pointer");
+  return nufft_plan_weights(d_kxy, n_samples, os, width, beta, d_ab, d_wts, (cudaStream_t)stream);
 }
 
 int tf_resample_axis(const float* d_in, float* d_out, long long outer, int n_src, int n_tgt,

@@ -291,6 +291,41 @@ k_nufft_cols(const c32* __restrict__ Tn, const float* __restrict__ deapod, int n
   }
 }
 
+// ============================================================ plan tables
+// Per sample m and axis: first window index a0 = ceil(eta - w/2) mod os with
+// eta = k os / (2 pi), and the w Kaiser-Bessel weights I0(beta sqrt(1 - (2x/w)^2))
+// at x = a0 + t - eta, in fp64 (the reference tabulates the same kernel,
+// nufft.py:80-87).  kxy: [S][2] fp64; ab: [S] int2; wts: [S][2w] fp32.
+__global__ void k_plan_weights(const double* __restrict__ kxy, long long S, int os, int w,
+                               double beta, int2* __restrict__ ab, float* __restrict__ wts) {
+  const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (m >= S) return;
+  int a0[2];
+#pragma unroll
+  for (int ax = 0; ax < 2; ++ax) {
+    const double eta = kxy[2 * m + ax] * os / (2.0 * 3.14159265358979323846);
+    const double start = ceil(eta - 0.5 * w);
+    long long st = (long long)start % os;
+    if (st < 0) st += os;
+    a0[ax] = (int)st;
+    for (int t = 0; t < w; ++t) {
+      const double x = start + t - eta;
+      const double arg = 1.0 - (2.0 * x / w) * (2.0 * x / w);
+      wts[m * 2 * w + ax * w + t] = arg >= 0.0 ? (float)cyl_bessel_i0(beta * sqrt(arg)) : 0.f;
+    }
+  }
+  ab[m] = make_int2(a0[0], a0[1]);
+}
+
+int nufft_plan_weights(const double* kxy, long long S, int os, int w, double beta, void* ab,
+                       float* wts, cudaStream_t st) {
+  if (S <= 0) return TF_OK;
+  const int bs = 256;
+  k_plan_weights<<<(unsigned)((S + bs - 1) / bs), bs, 0, st>>>(kxy, S, os, w, beta,
+                                                               reinterpret_cast<int2*>(ab), wts);
+  return check_launch("k_plan_weights");
+}
+
 // ============================================================ host dispatch
 namespace {
 

@@ -75,24 +75,34 @@ def gpu_grid_side(os_side: int) -> int:
 
 
 class PlanTables:
-    """Host (float64 -> fp32/int32 numpy) tables of one plan; see module docstring."""
+    """Host (float64 -> fp32/int32 numpy) tables of one plan; see module docstring.
 
-    def __init__(self, n: int, samples: np.ndarray, width: int, beta: float, os_side: int):
+    ``weights=False`` skips the Kaiser-Bessel weights (the device builds them,
+    csrc/nufft.cu k_plan_weights); the window starts, the tile CSR, the
+    deapodisation and the pre-phase are always built here."""
+
+    def __init__(self, n: int, samples: np.ndarray, width: int, beta: float, os_side: int,
+                 weights: bool = True):
         g = gpu_grid_side(os_side)
         self.side, self.width, self.beta = n, width, beta
         self.grid = g
         kx, ky = samples[:, 0], samples[:, 1]
 
-        def windows(k):
-            eta = k * g / (2.0 * np.pi)
-            start = np.ceil(eta - width / 2.0).astype(np.int64)
-            idx = start[:, None] + np.arange(width)[None, :]
-            return start % g, _kb(idx - eta[:, None], width, beta)
+        def start(k):
+            return np.ceil(k * g / (2.0 * np.pi) - width / 2.0).astype(np.int64)
 
-        a0, wx = windows(kx)
-        b0, wy = windows(ky)
+        def kb_weights(k, st):
+            eta = k * g / (2.0 * np.pi)
+            idx = st[:, None] + np.arange(width)[None, :]
+            return _kb(idx - eta[:, None], width, beta)
+
+        sa, sb = start(kx), start(ky)
+        a0, b0 = sa % g, sb % g
         self.ab = np.stack([a0, b0], axis=1).astype(np.int32)
-        self.wts = np.concatenate([wx, wy], axis=1).astype(np.float32)
+        self.wts = None
+        if weights:
+            self.wts = np.concatenate([kb_weights(kx, sa), kb_weights(ky, sb)],
+                                      axis=1).astype(np.float32)
         xprime = np.arange(n) - n // 2
         dk = kaiser_bessel_fourier(xprime / g, width, beta)
         floor = 1e-12 * np.max(np.abs(dk))
@@ -163,20 +173,37 @@ class NufftPlan:
 
     @property
     def tables(self) -> PlanTables:
+        """Host tables including the Kaiser-Bessel weights (numpy, float64 math)."""
         if self._tables is None:
             self._tables = PlanTables(self.grid_side, np.asarray(self.sampling.samples),
                                       self.kernel_width, self.kernel_params, self.os_side)
         return self._tables
 
     def device_tables(self) -> dict:
-        """fp32/int32 tables on the current CUDA device (built once per device)."""
+        """fp32/int32 tables on the current CUDA device (built once per device): the
+        window starts and Kaiser-Bessel weights by k_plan_weights (fp64 on the GPU),
+        the tile CSR / deapodisation / pre-phase from the host."""
         dev = _lib.device()
         t = self._device_tables.get(dev.index)
         if t is None:
-            h = self.tables
+            lib = _lib.ensure_ready()
+            samples = np.ascontiguousarray(self.sampling.samples, dtype=np.float64)
+            h = self._tables or PlanTables(self.grid_side, samples, self.kernel_width,
+                                           self.kernel_params, self.os_side, weights=False)
             up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+            kxy = up(samples)
+            ab = torch.empty((samples.shape[0], 2), dtype=torch.int32, device=dev)
+            wts = torch.empty((samples.shape[0], 2 * self.kernel_width), dtype=torch.float32,
+                              device=dev)
+            _lib.check(lib.tf_nufft_plan_weights(kxy.data_ptr(), samples.shape[0], self.gpu_side,
+                                                 self.kernel_width, float(self.kernel_params),
+                                                 ab.data_ptr(), wts.data_ptr(),
+                                                 _lib.stream_handle()), "tf_nufft_plan_weights")
+            # the tile CSR was binned from the host window starts: they must agree
+            if not np.array_equal(ab.cpu().numpy(), h.ab):
+                raise RuntimeError("NUFFT plan: device window starts differ from the host binning")
             t = {
-                "ab": up(h.ab), "wts": up(h.wts), "deapod": up(h.deapod),
+                "ab": ab, "wts": wts, "deapod": up(h.deapod),
                 "prephase": up(h.prephase.view(np.float32)),
                 "tile_ptr": up(h.tile_ptr), "tile_idx": up(h.tile_idx),
                 "sphase": None,

@@ -136,13 +136,13 @@ def back_project(p: NufftPlan, sino) -> ImageGrid:
     if rows.shape != (1, n_angles, nd):
         raise ValueError(f"expected single-slice sinogram of shape (1, {n_angles}, {nd})")
     img = back_project_stack(p, rows)
-    return ImageGrid(img[0].to("cpu", torch.float64).numpy())
+    return ImageGrid._owned(_device.to_host64(img[0]))
 
 
 def back_project_volume(p: NufftPlan, sino: Sinogram) -> Volume:
     """Adjoint projection of every slice of a stacked sinogram (radon.py:131-134)."""
     _sampling_matches(p, sino.angles, sino.detector_bins)
-    return Volume(back_project_stack(p, sino.data).to("cpu", torch.float64).numpy())
+    return Volume._owned(_device.to_host64(back_project_stack(p, sino.data)))
 
 
 def ramp_filter_apply(sino: Sinogram) -> Sinogram:
@@ -160,5 +160,5 @@ def fbp(p: NufftPlan, sino: Sinogram):
     """Filtered back-projection with the 1/(2P) scale (radon.py:145-160): an
     ImageGrid for a single slice, a Volume otherwise."""
     _sampling_matches(p, sino.angles, sino.detector_bins)
-    vol = fbp_stack(p, sino.data).to("cpu", torch.float64).numpy()
-    return ImageGrid(vol[0]) if vol.shape[0] == 1 else Volume(vol)
+    vol = _device.to_host64(fbp_stack(p, sino.data))
+    return ImageGrid._owned(vol[0]) if vol.shape[0] == 1 else Volume._owned(vol)

@@ -34,7 +34,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import _lib
+from . import _device, _lib
 from .geometry import ScanGeometry, Sinogram, Volume, polar_sampling
 from .nufft import NufftPlan
 from .qggmrf import stencil_2d, stencil_3d
@@ -256,7 +256,7 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
         if isinstance(vol, torch.Tensor):
             if gather == "none":
                 return vol, records
-            vol = Volume(vol.to("cpu", torch.float64).numpy())
+            vol = Volume._owned(_device.to_host64(vol))
         return vol, records
 
     rank = dist.get_rank(group)
@@ -288,7 +288,7 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
         if gather == "none":
             return slab, records
         full = comm.gather(slab, parts)
-        vol = Volume(full.to("cpu", torch.float64).numpy()) if rank == 0 else None
+        vol = Volume._owned(_device.to_host64(full)) if rank == 0 else None
         return vol, records
     except (TransportError, ValueError, FloatingPointError):
         raise

@@ -127,3 +127,12 @@ def test_sampling_mismatch_raises(tf):
     p = _plan(tf, ang, 32, 32)
     with pytest.raises(ValueError):
         tf.fbp(p, tf.Sinogram(angles=ang, data=np.zeros((12, 33))))
+
+
+def test_device_plan_weights_match_host(tf):
+    ang = np.linspace(0, np.pi, 40, endpoint=False)
+    p = _plan(tf, ang, 200, 100)
+    host = p.tables
+    dev = p.device_tables()
+    np.testing.assert_array_equal(dev["ab"].cpu().numpy(), host.ab)
+    np.testing.assert_allclose(dev["wts"].cpu().numpy(), host.wts, rtol=2e-6, atol=1e-6)
