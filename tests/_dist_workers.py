@@ -57,3 +57,27 @@ def solve_worker(rank, world, port, fixture, out_dir):
                      "nsnap": len(snaps)}, allow_pickle=True)
     finally:
         dist.destroy_process_group()
+
+
+def solve7_worker(rank, world, port, out_dir):
+    """7-slice problem (24^2, 12 angles) on cuda:0; W = world over gloo (W = 1: no group)."""
+    import paper_2603_28756_b200 as tf
+    from paper_2603_28756_b200.runtime import distributed_solve
+
+    torch.cuda.set_device(0)
+    if world > 1:
+        _init(rank, world, port)
+    try:
+        ang = np.linspace(0, np.pi, 12, endpoint=False)
+        g = np.random.default_rng(7).standard_normal((7, 12, 24))
+        sino = tf.Sinogram(angles=ang, data=g)
+        prm = tf.QggmrfParams(sigma=0.3, lam=0.05)
+        cfg = tf.SolverConfig(max_iters=6, tol=1e-300, lipschitz=300.0)
+        vol, recs = distributed_solve(sino, 24, prm, cfg, world)
+        if rank == 0:
+            np.save(os.path.join(out_dir, f"solve7_w{world}.npy"),
+                    {"vol": vol.data, "obj": np.array([r.objective for r in recs])},
+                    allow_pickle=True)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()

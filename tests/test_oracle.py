@@ -98,3 +98,19 @@ def test_partition_fixture():
         n, w = map(int, key.split("_"))
         assert np.array_equal(np.array(O.partition(n, w)), d[key])
     np.testing.assert_allclose(d["recon_w2"], d["recon_w1"], atol=1e-10)
+
+
+def test_c2_reduced_fixture():
+    """The oracle reproduces the reference's C2 (reduced, Poisson) run."""
+    d = golden("c2_reduced.npz")
+    n = d["f0"].shape[-1]
+    nd = d["g"].shape[2]
+    psf = O.build_psf(d["angles"], nd, n)
+    plan = O.make_plan(n, d["angles"], nd)
+    assert rel_l2(O.fbp(plan, d["g"]), d["f0"]) < 1e-12
+    rs = O.rstar(plan, d["g"])
+    pr = O.Prior(sigma=float(d["sigma"]), lam=5e-4)
+    rec, recs = O.solve(psf, rs, float(np.sum(d["g"] ** 2)), pr, d["f0"], 50, float(d["L"]),
+                        tol=1e-300)
+    assert rel_l2(rec, d["recon"]) < 1e-10
+    assert [r.restarted for r in recs] == list(d["restarted"])
