@@ -183,9 +183,21 @@ k_spread(const c32* __restrict__ c, long long c_stride, int nslices, int os, int
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[i][j] = mk(0.f, 0.f);
   const int beg = __ldg(tile_ptr + tile), end = __ldg(tile_ptr + tile + 1);
+  // one-sample-ahead software pipeline: the index chain tile_idx -> ab -> weights /
+  // values of sample q+1 is in flight while sample q accumulates
+  int m_n = 0;
+  int2 s_n = make_int2(0, 0);
+  if (beg < end) {
+    m_n = __ldg(tile_idx + beg);
+    s_n = __ldg(ab + m_n);
+  }
   for (int q = beg; q < end; ++q) {
-    const int m = __ldg(tile_idx + q);
-    const int2 s = __ldg(ab + m);
+    const int m = m_n;
+    const int2 s = s_n;
+    if (q + 1 < end) {
+      m_n = __ldg(tile_idx + q + 1);
+      s_n = __ldg(ab + m_n);
+    }
     int db = bb - s.y;
     if (db < 0) db += os;
     if (db >= W && db <= os - 4) continue;  // none of this warp's rows (warp-uniform)
