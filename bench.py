@@ -413,6 +413,12 @@ def _mbir_distributed(tf, z, world, rank, prm, L, timed, setup, per_it_local, bp
     (_, recs), t_total = timed(lambda: distributed_solve(sino, N_SIDE, prm, cfg, world,
                                                          gather="none"))
     step_ms = max_over_ranks(float(np.median([r.step_time for r in recs[1:]])) * 1e3, world)
+    from paper_2603_28756_b200.runtime import distributed_solve_hierarchical
+
+    hier = tf.GridHierarchy(levels=(512, 1024, 2048), iters_per_level=(40, 20, 10))
+    _, t_hier = timed(lambda: distributed_solve_hierarchical(
+        sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300, lipschitz=L), world,
+        use_fbp_init=True, gather="none"))
     return {
         "workload": f"z-slab MBIR: {z * world} x 2048^2 over {world} GPUs ({z} slices per GPU), "
                     "128 angles, Nd=2048, qGGMRF lam=5e-4",
@@ -420,6 +426,9 @@ def _mbir_distributed(tf, z, world, rank, prm, L, timed, setup, per_it_local, bp
         "solve_ms_per_iter_single_gpu_slab": per_it_local,
         "distributed_ms_per_iter": step_ms,
         "distributed_total_ms_incl_setup": t_total,
+        "hierarchical_3level_ms": t_hier,
+        "hierarchical_schedule": "levels (512, 1024, 2048), iterations (40, 20, 10), FBP init, "
+                                 "re-partitioned z-slabs per level, Lanczos-3 upsampling",
         "solve_bytes_per_voxel_iter": bpv,
         "solve_hbm_frac": bpv * z * N_SIDE * N_SIDE / (step_ms / 1e3) / 1e9 / peak,
         "comm_per_iter": "2 halo planes of 16.8 MB per interior boundary + one 3 x fp64 allreduce",

@@ -51,6 +51,7 @@ __all__ = [
     "partition",
     "exchange_halos",
     "distributed_solve",
+    "distributed_solve_hierarchical",
 ]
 
 
@@ -197,6 +198,18 @@ class SlabComm:
         dist.broadcast(t, src=self._peer(root), group=self.group)
         return float(t.item())
 
+    def allgather(self, slab: torch.Tensor, parts) -> torch.Tensor:
+        """The full volume on every rank (slabs padded to the largest size)."""
+        big = max(p.size for p in parts)
+        dev = slab.device if (self.direct and slab.is_cuda) else torch.device("cpu")
+        pad = torch.zeros((big,) + tuple(slab.shape[1:]), dtype=slab.dtype, device=dev)
+        pad[:slab.shape[0]] = slab.to(dev)
+        bufs = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(bufs, pad, group=self.group)
+        self.counts["allgather"] += 1
+        full = torch.cat([bufs[p.worker_id][:p.size] for p in parts])
+        return full.to(slab.device)
+
     def gather(self, slab: torch.Tensor, parts, root: int = 0):
         """Full volume on ``root`` (None elsewhere); slabs padded to the largest size."""
         big = max(p.size for p in parts)
@@ -294,3 +307,89 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
         raise
     except Exception as exc:  # noqa: BLE001 - same contract as runtime.py:688-690
         raise RuntimeError(f"worker {rank} failed: {exc}") from exc
+
+
+def distributed_solve_hierarchical(full_sino: Sinogram, hierarchy, params, cfg: SolverConfig,
+                                   n_workers: int, *, use_fbp_init: bool = False,
+                                   downsample_angles: bool = False,
+                                   nufft_tolerance: float = 1e-6, oversampling: float = 2.0,
+                                   on_record=None, gather: str = "root", group=None):
+    """Coarse-to-fine schedule over z-slabs (multires.py:198-242 x runtime.py:622-691).
+
+    The reference never combines the two (cli.py:104-131); the north-star C4/C5
+    runs need both.  Each level is re-partitioned (coarse and fine slabs do not
+    nest), the level's sinogram rows of the slab are strided on the host, and the
+    level solves with the slab loop of ``distributed_solve``.  Between levels the
+    coarse estimate is all-gathered once (one-time per level) and every rank
+    upsamples only its fine slab, so the Lanczos z-taps across slab boundaries
+    see exactly the single-GPU inputs.  Returns ``(volume, per-level records)``
+    as ``solve_hierarchical`` (volume on rank 0 with ``gather="root"``).
+    """
+    from .multires import _strided_indices, upsample_slab
+    from .radon import fbp_stack
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if n_workers != world:
+        raise ValueError(f"n_workers={n_workers} must equal the process-group size {world}")
+    if world == 1:
+        from .multires import solve_hierarchical
+
+        return solve_hierarchical(full_sino, hierarchy, params, cfg, use_fbp_init=use_fbp_init,
+                                  downsample_angles=downsample_angles,
+                                  nufft_tolerance=nufft_tolerance, oversampling=oversampling,
+                                  on_record=on_record)
+    target = hierarchy.levels[-1]
+    if full_sino.detector_bins < target:
+        raise ValueError("detector does not cover the target grid")
+    rank = dist.get_rank(group)
+    n_levels = len(hierarchy.levels)
+    all_records, estimate, parts_prev = [], None, None
+    for lvl, side in enumerate(hierarchy.levels):
+        factor = 1 << (n_levels - 1 - lvl)
+        bins = _strided_indices(full_sino.detector_bins, factor) if factor > 1 else None
+        zidx = (_strided_indices(full_sino.slices, factor)
+                if factor > 1 and full_sino.slices > 1 else np.arange(full_sino.slices))
+        angles = full_sino.angles
+        keep = np.arange(0, angles.size, factor) if (downsample_angles and factor > 1) else None
+        if keep is not None:
+            angles = angles[keep]
+        n_z = zidx.size
+        if n_z < n_workers:
+            raise ValueError(f"level {lvl} has {n_z} slices for {n_workers} workers")
+        parts = partition(n_z, n_workers)
+        part = parts[rank]
+        rows = full_sino.data[zidx[part.begin:part.end]]
+        if bins is not None:
+            rows = rows[:, :, bins] / factor
+        if keep is not None:
+            rows = rows[:, keep, :]
+        nd = rows.shape[2]
+        geom = ScanGeometry(angles=angles, detector_bins=nd, image_side=side)
+        sampling = polar_sampling(geom)
+        plan = NufftPlan(side, sampling, nufft_tolerance, oversampling)
+        psf = build_psf(sampling, side, nufft_tolerance, oversampling)
+        comm = SlabComm(part, group)
+        L = cfg.lipschitz
+        if L is None:
+            L = comm.broadcast_scalar(estimate_lipschitz(psf, params) if rank == 0 else None)
+        ctx = FidelityContext(psf=psf, rstar=back_project_stack(plan, rows),
+                              g_norm_sq=float(np.sum(rows ** 2)))
+        if estimate is None:
+            x0 = (fbp_stack(plan, rows) if use_fbp_init else
+                  torch.zeros((part.size, side, side), device=_lib.device()))
+        else:
+            coarse = SlabComm(parts_prev[rank], group).allgather(estimate, parts_prev)
+            x0 = upsample_slab(coarse, side, n_z, part.begin, part.end)
+        cfg_l = SolverConfig(max_iters=hierarchy.iters_per_level[lvl], tol=cfg.tol, lipschitz=L,
+                             restart=cfg.restart, log_every=cfg.log_every, nonneg=cfg.nonneg)
+        sink = ((lambda rec, _l=lvl: on_record(_l, rec))
+                if (on_record is not None and rank == 0) else None)
+        stencil = stencil_3d() if n_z > 1 else stencil_2d()
+        estimate, records = _iterate(ctx, params, cfg_l, x0, stencil, L, comm=comm, on_record=sink)
+        all_records.append(records)
+        parts_prev = parts
+    if gather == "none":
+        return estimate, all_records
+    full = SlabComm(parts_prev[rank], group).gather(estimate, parts_prev)
+    vol = Volume._owned(_device.to_host64(full)) if rank == 0 else None
+    return vol, all_records

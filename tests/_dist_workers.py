@@ -81,3 +81,26 @@ def solve7_worker(rank, world, port, out_dir):
     finally:
         if world > 1:
             dist.destroy_process_group()
+
+
+def hier_worker(rank, world, port, fixture, out_dir):
+    """distributed_solve_hierarchical on cuda:0 (gloo) for the hier.npz problem."""
+    import paper_2603_28756_b200 as tf
+    from paper_2603_28756_b200.runtime import distributed_solve_hierarchical
+
+    torch.cuda.set_device(0)
+    _init(rank, world, port)
+    try:
+        d = dict(np.load(fixture))
+        sino = tf.Sinogram(angles=d["angles"], data=d["g"])
+        prm = tf.QggmrfParams(sigma=0.1, lam=1e-2)
+        hier = tf.GridHierarchy(levels=(16, 32), iters_per_level=(6, 4))
+        vol, lrecs = distributed_solve_hierarchical(sino, hier, prm,
+                                                    tf.SolverConfig(max_iters=1, tol=1e-300),
+                                                    world, use_fbp_init=True)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "hier.npy"),
+                    {"vol": vol.data, "obj0": np.array([r.objective for r in lrecs[0]]),
+                     "obj1": np.array([r.objective for r in lrecs[1]])}, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()

@@ -60,3 +60,22 @@ def test_worker_count_must_match_group(tf):
         distributed_solve(sino, 16, tf.QggmrfParams(sigma=0.3), tf.SolverConfig(max_iters=1), 2)
     with pytest.raises(ValueError):
         distributed_solve(sino, 16, tf.QggmrfParams(sigma=0.3), tf.SolverConfig(max_iters=1), 7)
+
+
+def test_hierarchical_over_slabs_matches_reference(tf, tmp_path):
+    """Multires x z-slabs (W = 2 on one GPU) against the reference's single-worker
+    hierarchical run (hier.npz): levels (16, 32), FBP init, 2 -> 4 slices."""
+    import torch.multiprocessing as mp
+
+    from _dist_workers import hier_worker
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(hier_worker, args=(2, port, str(GOLDEN / "hier.npz"), str(tmp_path)), nprocs=2,
+             join=True)
+    r = np.load(tmp_path / "hier.npy", allow_pickle=True).item()
+    d = golden("hier.npz")
+    assert rel_l2(r["vol"], d["recon"]) < 1e-3
+    np.testing.assert_allclose(r["obj0"], d["obj0"], rtol=1e-4)
+    np.testing.assert_allclose(r["obj1"], d["obj1"], rtol=1e-4)
