@@ -165,7 +165,7 @@ def cpu_sample(threads: int | None = None, slices: int | None = None, repeats: i
     """Reference algorithm (oracle port of toeplitz._apply_batch) on host cores."""
     import oracle as O
 
-    threads = threads or os.cpu_count() or 1
+    threads = threads or min(32, os.cpu_count() or 1)  # ~1.2 GB of complex128 per thread
     slices = slices or threads
     psf = O.build_psf(angles(), N_BINS, N_SIDE)
     rng = np.random.default_rng(0)
@@ -184,7 +184,7 @@ def run_reference(args, world, rank):
         return
     import oracle as O
 
-    threads = os.cpu_count() or 1
+    threads = min(32, os.cpu_count() or 1)  # ~1.2 GB of complex128 scratch per thread
     psf = O.build_psf(angles(), N_BINS, N_SIDE)
     rng = np.random.default_rng(0)
     x = rng.standard_normal((threads, N_SIDE, N_SIDE))

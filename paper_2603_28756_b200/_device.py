@@ -88,14 +88,22 @@ def to_device(arr: np.ndarray) -> torch.Tensor:
 
 
 def to_host64(t: torch.Tensor) -> np.ndarray:
-    """fp32 device tensor -> float64 host array (widened on the device, chunked)."""
-    out = np.empty(tuple(t.shape), dtype=np.float64)
-    dst = torch.from_numpy(out).reshape(-1)
+    """fp32 device tensor -> float64 host array (widened on the device, chunked).
+
+    The result lives in page-locked memory from torch's caching host allocator
+    (the returned array keeps its tensor alive), so the device->host copy runs
+    at full link speed and repeated calls reuse the pinned block."""
+    try:
+        out = torch.empty(tuple(t.shape), dtype=torch.float64, pin_memory=True)
+    except RuntimeError:  # pinned memory exhausted: pageable fallback of the host buffer
+        out = torch.empty(tuple(t.shape), dtype=torch.float64)
+    dst = out.reshape(-1)
     src = t.detach().reshape(-1)
     for lo in range(0, src.numel(), _CHUNK_ELEMS):
         hi = min(src.numel(), lo + _CHUNK_ELEMS)
-        dst[lo:hi].copy_(src[lo:hi].to(torch.float64))
-    return out
+        dst[lo:hi].copy_(src[lo:hi].to(torch.float64), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out.numpy()
 
 
 def wrap_like(kind: str, t: torch.Tensor):

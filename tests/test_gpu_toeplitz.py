@@ -119,3 +119,15 @@ def test_device_tensor_path(tf):
     assert isinstance(y, torch.Tensor) and y.is_cuda and y.shape == x.shape
     ref = tf.toeplitz_apply(psf, x.double().cpu().numpy())
     assert rel_l2(y.double().cpu().numpy(), ref) < 1e-6
+
+
+def test_repeated_apply_bitwise_stable(tf):
+    """Async-race guard (TMA ring, bulk prefetch): 2048^2 applies repeated bit for bit."""
+    import torch
+
+    n = 2048
+    psf = _psf(tf, np.linspace(0, np.pi, 16, endpoint=False), n, n)
+    x = torch.randn((3, n, n), device="cuda", generator=torch.Generator("cuda").manual_seed(0))
+    ref = tf.toeplitz_apply(psf, x).clone()
+    for _ in range(10):
+        assert torch.equal(tf.toeplitz_apply(psf, x), ref)
