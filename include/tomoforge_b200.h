@@ -138,6 +138,24 @@ int tf_nufft_type1(const void* d_samples, long long sample_stride, long long nsl
 int tf_nufft_plan_weights(const double* d_kxy, long long n_samples, int os, int width,
                           double beta, void* d_ab, float* d_wts, void* stream);
 
+/* ---- forward projector --------------------------------
+ * Type-2 NUFFT (nufft.type2, nufft.py:184-200) of nslices real N x N images:
+ * deapodise, half spectrum of the offset-0 embedding on the os x os grid, then
+ * per sample the width x width window gathered with the Kaiser-Bessel weights
+ * and the conjugate pre-phase; d_out[z][m] (complex64) = that sum times
+ * d_factor[m] (complex64, NULL = 1).  Tables as for tf_nufft_type1. */
+long long tf_nufft_type2_workspace_bytes(int n, int os, long long nslices);
+int tf_nufft_type2(const float* d_image, long long nslices, int n, int os, int width,
+                   const void* d_ab, const float* d_wts, const void* d_prephase,
+                   const float* d_deapod, const void* d_factor, long long n_samples, void* d_out,
+                   void* d_ws, long long ws_bytes, void* stream);
+
+/* Real parts of the inverse DFTs of nrows complex rows given in signed-frequency
+ * order (the ifftshift + ifft of radon.forward_project, radon.py:91-96), times
+ * scale: d_out fp32 [nrows][nd]. */
+int tf_detector_rows_inv(const void* d_samples, long long nrows, int nd, float scale,
+                         float* d_out, void* stream);
+
 /* ---- Lanczos-3 resampling (K9) ----------------------------------------------
  * One axis of the separable upsampler of multires.upsample (multires.py:145-195):
  *   d_out[o][t][i] = sum_{k < taps} d_weights[t][k] * d_in[o][d_start[t] + k][i]

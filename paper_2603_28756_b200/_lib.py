@@ -55,6 +55,10 @@ _SIGNATURES = {
                        + [_c_float, _c_int, _c_void_p, _c_void_p, _c_ll, _c_void_p]),
     "tf_nufft_plan_weights": (_c_int, [_c_void_p, _c_ll, _c_int, _c_int, _c_double, _c_void_p,
                                        _c_void_p, _c_void_p]),
+    "tf_nufft_type2_workspace_bytes": (_c_ll, [_c_int, _c_int, _c_ll]),
+    "tf_nufft_type2": (_c_int, [_c_void_p, _c_ll, _c_int, _c_int, _c_int] + [_c_void_p] * 5
+                       + [_c_ll, _c_void_p, _c_void_p, _c_ll, _c_void_p]),
+    "tf_detector_rows_inv": (_c_int, [_c_void_p, _c_ll, _c_int, _c_float, _c_void_p, _c_void_p]),
     "tf_resample_axis": (_c_int, [_c_void_p, _c_void_p, _c_ll, _c_int, _c_int, _c_ll, _c_void_p,
                                   _c_void_p, _c_int, _c_void_p]),
     "tf_timing_enable": (_c_int, [_c_int]),

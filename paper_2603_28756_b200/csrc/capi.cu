@@ -116,6 +116,12 @@ int energy_fid(const float* fn, const float* fn_hi, const float* f, const float*
 int dot2(const float* x, const float* a, const float* b, long long n, double* out, double* ws,
          cudaStream_t st);
 size_t nufft_workspace_bytes(int os, long long nslices);
+size_t type2_workspace_bytes(int n, int os, long long nslices);
+int nufft_type2(const float* img, long long nslices, int n, int os, int w, const void* ab,
+                const float* wts, const void* preph, const float* deapod, const void* factor,
+                long long n_samples, void* out, void* ws, size_t ws_bytes, cudaStream_t st);
+int detector_rows_inv(const void* c, long long nrows, int nd, float gain, float* out,
+                      cudaStream_t st);
 int nufft_plan_weights(const double* kxy, long long S, int os, int w, double beta, void* ab,
                        float* wts, cudaStream_t st);
 int resample_axis(const float* in, float* out, long long outer, int n_src, int n_tgt,
@@ -270,6 +276,31 @@ int tf_nufft_plan_weights(const double* d_kxy, long long n_samples, int os, int 
   if (n_samples < 0 || os < 2 || width < 2 || width > 16) return fail_arg("bad plan arguments");
   if (n_samples > 0 && (!d_kxy || !d_ab || !d_wts)) return fail_arg("null pointer");
   return nufft_plan_weights(d_kxy, n_samples, os, width, beta, d_ab, d_wts, (cudaStream_t)stream);
+}
+
+long long tf_nufft_type2_workspace_bytes(int n, int os, long long nslices) {
+  if (n < 1 || os < 2 || nslices < 0) return fail_arg("bad type2 workspace query");
+  return (long long)type2_workspace_bytes(n, os, nslices);
+}
+
+int tf_nufft_type2(const float* d_image, long long nslices, int n, int os, int width,
+                   const void* d_ab, const float* d_wts, const void* d_prephase,
+                   const float* d_deapod, const void* d_factor, long long n_samples, void* d_out,
+                   void* d_ws, long long ws_bytes, void* stream) {
+  TF_TRY(ensure_init());
+  if (nslices < 0 || n < 1 || n_samples < 0) return fail_arg("bad type2 shape");
+  if (nslices == 0 || n_samples == 0) return TF_OK;
+  if (!d_image || !d_ab || !d_wts || !d_prephase || !d_deapod || !d_out || !d_ws)
+    return fail_arg("null pointer");
+  return nufft_type2(d_image, nslices, n, os, width, d_ab, d_wts, d_prephase, d_deapod, d_factor,
+                     n_samples, d_out, d_ws, (size_t)ws_bytes, (cudaStream_t)stream);
+}
+
+int tf_detector_rows_inv(const void* d_samples, long long nrows, int nd, float scale,
+                         float* d_out, void* stream) {
+  TF_TRY(ensure_init());
+  if (nrows < 0 || (nrows > 0 && (!d_samples || !d_out))) return fail_arg("bad arguments");
+  return detector_rows_inv(d_samples, nrows, nd, scale, d_out, (cudaStream_t)stream);
 }
 
 int tf_resample_axis(const float* d_in, float* d_out, long long outer, int n_src, int n_tgt,

@@ -338,6 +338,100 @@ int nufft_plan_weights(const double* kxy, long long S, int os, int w, double bet
   return check_launch("k_plan_weights");
 }
 
+// ============================================================ forward NUFFT (type 2)
+// Reference: nufft.type2 (nufft.py:184-200): deapodise, embed centred, fft2,
+// gather each sample's w x w window with the Kaiser-Bessel weights, x phase;
+// radon.forward_project (radon.py:85-96): x detector phase, ifftshift, ifft
+// along the bins, real part.  Here the image (x deapod) is transformed with the
+// Toeplitz row kernel and a forward column pass into the half spectrum
+// S[b][a] (b in [0, os/2]) of its offset-0 embedding; the centring is the
+// conjugate pre-phase per grid index, and G(a, b) for b > os/2 is
+// conj(G(-a, -b)) (real image).  One thread per (sample, slice) gathers its
+// window from L2.
+
+// x * deapod[ix] * deapod[iy] * gain  (fp32, same layout)
+__global__ void k_scale_deapod(const float* __restrict__ x, float* __restrict__ out, long long total,
+                               int n, const float* __restrict__ deapod, float gain) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int iy = (int)(i % n);
+    const int ix = (int)((i / n) % n);
+    out[i] = x[i] * __ldg(deapod + ix) * __ldg(deapod + iy) * gain;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256)
+k_interp(const c32* __restrict__ S, int os, long long n_samples, const int2* __restrict__ ab,
+         const float* __restrict__ wts, const c32* __restrict__ preph,
+         const c32* __restrict__ factor, c32* __restrict__ out) {
+  const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (m >= n_samples) return;
+  const int z = blockIdx.y;
+  const int H = os / 2 + 1;
+  const c32* Sz = S + (long long)z * H * os;
+  const int2 s = __ldg(ab + m);
+  const float* wr = wts + m * (2 * W);
+  c32 wx[W];
+  int ax[W];
+#pragma unroll
+  for (int t = 0; t < W; ++t) {
+    int a = s.x + t;
+    if (a >= os) a -= os;
+    ax[t] = a;
+    wx[t] = scale(conj(__ldg(preph + a)), __ldg(wr + t));
+  }
+  c32 acc = mk(0.f, 0.f);
+#pragma unroll
+  for (int u = 0; u < W; ++u) {
+    int b = s.y + u;
+    if (b >= os) b -= os;
+    const c32 wy = scale(conj(__ldg(preph + b)), __ldg(wr + W + u));
+    c32 row = mk(0.f, 0.f);
+    if (b <= os / 2) {
+      const c32* Sb = Sz + (long long)b * os;
+#pragma unroll
+      for (int t = 0; t < W; ++t) row = cadd(row, cmul(__ldg(Sb + ax[t]), wx[t]));
+    } else {  // Hermitian mirror of a real image's spectrum
+      const c32* Sb = Sz + (long long)(os - b) * os;
+#pragma unroll
+      for (int t = 0; t < W; ++t) {
+        const int am = ax[t] == 0 ? 0 : os - ax[t];
+        row = cadd(row, cmul(conj(__ldg(Sb + am)), wx[t]));
+      }
+    }
+    acc = cadd(acc, cmul(row, wy));
+  }
+  if (factor) acc = cmul(acc, __ldg(factor + m));
+  out[(long long)z * n_samples + m] = acc;
+}
+
+// rows[r][n] = Re(ifft(ifftshift(c[r][.])))[n] * gain: c in signed-frequency
+// order (jj), complex; inverse mixed-radix DFT in shared memory (K8's engine)
+__global__ void k_detector_rows_inv(const c32* __restrict__ c, int nd, int L, int r, float gain,
+                                    float* __restrict__ out) {
+  extern __shared__ __align__(16) c32 sm[];
+  c32* a = sm;
+  c32* b = a + nd;
+  c32* cc = b + nd;
+  c32* tw = cc + nd;
+  const long long row = blockIdx.x;
+  const c32* x = c + row * nd;
+  const int jlo = -(nd / 2);
+  for (int q = threadIdx.x; q < nd; q += blockDim.x) {
+    float sn, co;
+    sincospif(2.0f * (float)q / (float)nd, &sn, &co);  // inverse: e^{+2 pi i q / nd}
+    tw[q] = mk(co, sn);
+    const int j = q + jlo;                               // signed index of entry q
+    a[j < 0 ? j + nd : j] = __ldg(x + q);                // ifftshift
+  }
+  __syncthreads();
+  c32* X = smem_dft(a, b, cc, tw, L, r, nd);
+  float* o = out + row * nd;
+  const float g = gain / (float)nd;
+  for (int k = threadIdx.x; k < nd; k += blockDim.x) o[k] = X[k].x * g;
+}
+
 // ============================================================ host dispatch
 namespace {
 
@@ -426,6 +520,73 @@ int dispatch_grid_fft(int os, const c32* grid, c32* Tn, long long nz, int n, con
 }
 
 }  // namespace
+
+size_t spectrum_workspace_bytes(int n, int M);
+int real_spectrum(const float* img, long long nslices, int n, int M, void* T, void* S,
+                  cudaStream_t st);
+
+size_t type2_workspace_bytes(int n, int os, long long nslices) {
+  const size_t spec = (size_t)(os / 2 + 1) * os * sizeof(c32);
+  return (size_t)nslices * (spec + spectrum_workspace_bytes(n, os) + (size_t)n * n * sizeof(float));
+}
+
+template <int W>
+int launch_interp(const c32* S, int os, long long ns, long long nz, const int2* ab,
+                  const float* wts, const c32* preph, const c32* factor, c32* out,
+                  cudaStream_t st) {
+  const dim3 g((unsigned)((ns + 255) / 256), (unsigned)nz);
+  k_interp<W><<<g, 256, 0, st>>>(S, os, ns, ab, wts, preph, factor, out);
+  return check_launch("k_interp");
+}
+
+int nufft_type2(const float* img, long long nslices, int n, int os, int w, const void* ab,
+                const float* wts, const void* preph, const float* deapod, const void* factor,
+                long long n_samples, void* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!is_pow2(os) || os < 32 || os > 8192 || 2 * n > os)
+    return fail_arg("NUFFT grid side %d unsupported for N = %d", os, n);
+  const size_t per = type2_workspace_bytes(n, os, 1);
+  const long long chunk = (long long)(ws_bytes / per);
+  if (chunk < 1) return fail_arg("type2 workspace too small: %zu < %zu", ws_bytes, per);
+  const long long spec = (long long)(os / 2 + 1) * os;
+  const long long nn = (long long)n * n;
+  for (long long z0 = 0; z0 < nslices; z0 += chunk) {
+    const long long nz = std::min(chunk, nslices - z0);
+    c32* S = reinterpret_cast<c32*>(ws);
+    c32* T = S + nz * spec;
+    float* sc = reinterpret_cast<float*>(reinterpret_cast<char*>(T) +
+                                         nz * spectrum_workspace_bytes(n, os));
+    const long long tot = nz * nn;
+    k_scale_deapod<<<(unsigned)std::min<long long>((tot + 255) / 256, 65535 * 8), 256, 0, st>>>(
+        img + z0 * nn, sc, tot, n, deapod, 1.f);
+    TF_TRY(check_launch("k_scale_deapod"));
+    TF_TRY(real_spectrum(sc, nz, n, os, T, S, st));
+    c32* o = reinterpret_cast<c32*>(out) + z0 * n_samples;
+    const int2* ab2 = reinterpret_cast<const int2*>(ab);
+    const c32* pp = reinterpret_cast<const c32*>(preph);
+    const c32* fc = reinterpret_cast<const c32*>(factor);
+    switch (w) {
+#define TF_W(W) case W: TF_TRY(launch_interp<W>(S, os, n_samples, nz, ab2, wts, pp, fc, o, st)); break;
+      TF_W(2) TF_W(3) TF_W(4) TF_W(5) TF_W(6) TF_W(7) TF_W(8) TF_W(9) TF_W(10) TF_W(11) TF_W(12)
+      TF_W(13) TF_W(14) TF_W(15) TF_W(16)
+#undef TF_W
+      default: return fail_arg("unsupported kernel width %d", w);
+    }
+  }
+  return TF_OK;
+}
+
+int detector_rows_inv(const void* c, long long nrows, int nd, float gain, float* out,
+                      cudaStream_t st) {
+  if (nd < 1 || nd > 8192) return fail_arg("detector bins %d outside [1, 8192]", nd);
+  int L = 1;
+  while ((nd % (2 * L)) == 0) L *= 2;
+  const size_t smem = 4 * (size_t)nd * sizeof(c32);
+  TF_TRY(prep_nufft_kernel(k_detector_rows_inv, smem));
+  if (nrows == 0) return TF_OK;
+  k_detector_rows_inv<<<(unsigned)nrows, 256, smem, st>>>(reinterpret_cast<const c32*>(c), nd, L,
+                                                          nd / L, gain, out);
+  return check_launch("k_detector_rows_inv");
+}
 
 int init_twiddles_nufft() { return check_cuda(init_twiddles_tu(), "twiddle init (nufft)"); }
 

@@ -957,7 +957,30 @@ struct PsfFn {
   }
 };
 
+// Half spectrum of real images for the forward NUFFT (type2): K1 over the N rows
+// (zero padded to M), then the forward column FFT of the M/2+1 half-spectrum
+// columns: S[z][ky][kx], ky in [0, M/2], kx in [0, M).
+template <int M>
+struct SpectrumFn {
+  static int run(const float* img, long long nslices, int n, c32* T, c32* S, cudaStream_t st) {
+    const long long img_sz = (long long)n * n;
+    TF_TRY(launch_rows_fwd<M>(img, T, n, n, img_sz, n, nslices, st));
+    return launch_cols_fwd<M>(T, S, n, nslices, st);
+  }
+};
+
 }  // namespace
+
+size_t spectrum_workspace_bytes(int n, int M) {
+  return (size_t)(M / 2 + 1) * RB * nrb_of(n) * sizeof(c32);  // row pass output per slice
+}
+
+int real_spectrum(const float* img, long long nslices, int n, int M, void* T, void* S,
+                  cudaStream_t st) {
+  if (2 * n > M) return fail_arg("spectrum side %d < 2N = %d", M, 2 * n);
+  return dispatch_m<SpectrumFn>(M, img, nslices, n, reinterpret_cast<c32*>(T),
+                                reinterpret_cast<c32*>(S), st);
+}
 
 int toeplitz_apply(const float* x, float* out, const float* aux, float alpha, float beta,
                    long long nslices, int n, int M, const void* PQ, const float* Bi, bool flip,

@@ -3,8 +3,8 @@
 Drop-in for the parts of tomoforge/nufft.py on the reconstruction path:
 ``NufftPlan`` / ``plan`` (nufft.py:104-176), ``type1`` (:203-223),
 ``kernel_width_for_tolerance`` (:54-57) and ``kaiser_bessel_fourier``
-(:90-101).  The forward transform ``type2`` (data synthesis only) is out of
-scope.
+(:90-101).  The forward transform ``type2`` (data synthesis)
+runs on the same tables through ``type2_stack`` (csrc/nufft.cu, k_interp).
 
 The plan keeps the reference's kernel width and shape parameter; its device
 tables are built once per (plan, device) on the host in float64:
@@ -34,6 +34,7 @@ __all__ = [
     "NufftPlan",
     "plan",
     "type1",
+    "type2",
     "kernel_width_for_tolerance",
     "kaiser_bessel_fourier",
 ]
@@ -226,6 +227,23 @@ class NufftPlan:
         return t["sphase"]
 
 
+    def sample_factor(self, kind: str) -> torch.Tensor:
+        """Per-sample complex64 factor on the device: ``"type2"`` = the plan phase
+        e^{-i (kx+ky) delta} (nufft.py:199); ``"project"`` = that times the detector
+        phase e^{-i w_j (Nd-1)/2} (radon.py:90)."""
+        t = self.device_tables()
+        key = "f_" + kind
+        if t.get(key) is None:
+            ph = self._phase
+            if kind == "project":
+                nd = self.sampling.radial_count
+                w = np.repeat(self.sampling.radial_freqs[None], self.sampling.angles.size,
+                              0).ravel()
+                ph = ph * np.exp(-1j * w * (nd - 1) / 2.0)
+            t[key] = torch.from_numpy(ph.astype(np.complex64).view(np.float32)).to(_lib.device())
+        return t[key]
+
+
 def plan(grid_side: int, sampling: PolarSampling, tolerance: float,
          oversampling: float = 2.0) -> NufftPlan:
     """nufft.py:171-176"""
@@ -272,3 +290,34 @@ def type1(p: NufftPlan, samples) -> np.ndarray:
     out = type1_stack(p, d, complex_out=True)
     return out[0].cpu().numpy().astype(np.complex128)
 
+
+
+def type2_stack(p: NufftPlan, images: torch.Tensor, factor: str = "type2") -> torch.Tensor:
+    """(Z, N, N) fp32 device images -> (Z, S) complex64 samples (type2 x factor)."""
+    lib = _lib.ensure_ready()
+    t = p.device_tables()
+    n, g = p.grid_side, p.gpu_side
+    if images.dim() != 3 or tuple(images.shape[1:]) != (n, n):
+        raise ValueError(f"image shape {tuple(images.shape[1:])} does not match plan grid {n}x{n}")
+    x = images.to(torch.float32).contiguous()
+    z = x.shape[0]
+    out = torch.empty((z, p.sample_count), dtype=torch.complex64, device=x.device)
+    per = lib.tf_nufft_type2_workspace_bytes(n, g, 1)
+    chunk = max(1, min(z, _WS_BYTES // per))
+    ws = _device.workspace(per * chunk, tag="nufft2")
+    fac = p.sample_factor(factor)
+    _lib.check(lib.tf_nufft_type2(
+        x.data_ptr(), z, n, g, p.kernel_width, t["ab"].data_ptr(), t["wts"].data_ptr(),
+        t["prephase"].data_ptr(), t["deapod"].data_ptr(), fac.data_ptr(), p.sample_count,
+        out.data_ptr(), ws.data_ptr(), per * chunk, _lib.stream_handle()), "tf_nufft_type2")
+    return out
+
+
+def type2(p: NufftPlan, image) -> np.ndarray:
+    """Grid -> polar samples c_m = sum_n f[n] exp(-i k_m . x_n) (nufft.py:184-200)."""
+    arr = image.data if isinstance(image, ImageGrid) else np.asarray(image)
+    n = p.grid_side
+    if arr.shape != (n, n):
+        raise ValueError(f"image shape {arr.shape} does not match plan grid {n}x{n}")
+    out = type2_stack(p, _device.to_device(np.asarray(arr, dtype=np.float64)[None]))
+    return out[0].cpu().numpy().astype(np.complex128)

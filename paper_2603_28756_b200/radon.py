@@ -3,8 +3,9 @@
 Drop-in for the reconstruction-side half of tomoforge/radon.py:
 ``back_project`` (radon.py:112-121), ``back_project_volume`` (:131-134),
 ``ramp_filter`` / ``RampFilter`` (:37-52), ``ramp_filter_apply`` (:137-142) and
-``fbp`` (:145-160).  The forward projector (data synthesis) is out of scope
-(SURVEY.md §8f).
+``fbp`` (:145-160).  The forward projector (``forward_project`` / ``project_volume``,
+radon.py:85-100) is the type-2 NUFFT followed by an
+inverse detector DFT (k_detector_rows_inv).
 
 Every (slice, angle) row goes through K8 (csrc/nufft.cu, k_detector_rows): a
 shared-memory DFT of length Nd, the fftshift, the detector-centring phase, 1/Nd,
@@ -25,7 +26,7 @@ import torch
 
 from . import _device, _lib
 from .geometry import ImageGrid, Sinogram, Volume, radial_frequencies
-from .nufft import NufftPlan, type1_stack
+from .nufft import NufftPlan, type1_stack, type2_stack
 
 __all__ = [
     "RampFilter",
@@ -36,6 +37,9 @@ __all__ = [
     "back_project_stack",
     "fbp",
     "fbp_stack",
+    "forward_project",
+    "forward_project_stack",
+    "project_volume",
 ]
 
 _ROW_CHUNK_BYTES = 1 << 30
@@ -162,3 +166,31 @@ def fbp(p: NufftPlan, sino: Sinogram):
     _sampling_matches(p, sino.angles, sino.detector_bins)
     vol = _device.to_host64(fbp_stack(p, sino.data))
     return ImageGrid._owned(vol[0]) if vol.shape[0] == 1 else Volume._owned(vol)
+
+
+def forward_project_stack(p: NufftPlan, images) -> torch.Tensor:
+    """(Z, N, N) images -> (Z, P, Nd) fp32 device projection rows (radon.py:85-96 per slice)."""
+    lib = _lib.ensure_ready()
+    x = images if isinstance(images, torch.Tensor) else _device.to_device(
+        np.asarray(images, dtype=np.float64))
+    if x.dim() == 2:
+        x = x[None]
+    samples = type2_stack(p, x.to(_lib.device()), factor="project")
+    n_ang, nd = p.sampling.angles.size, p.sampling.radial_count
+    rows = torch.empty((x.shape[0], n_ang, nd), dtype=torch.float32, device=samples.device)
+    _lib.check(lib.tf_detector_rows_inv(samples.data_ptr(), x.shape[0] * n_ang, nd, 1.0,
+                                        rows.data_ptr(), _lib.stream_handle()),
+               "tf_detector_rows_inv")
+    return rows
+
+
+def forward_project(p: NufftPlan, image) -> Sinogram:
+    """Parallel-beam projection of one slice (radon.py:85-96)."""
+    arr = image.data if isinstance(image, ImageGrid) else np.asarray(image, dtype=np.float64)
+    rows = forward_project_stack(p, arr[None])
+    return Sinogram(angles=p.sampling.angles, data=_device.to_host64(rows))
+
+
+def project_volume(p: NufftPlan, vol: Volume) -> Sinogram:
+    """Slice-by-slice forward projection of a volume (radon.py:99-103)."""
+    return Sinogram(angles=p.sampling.angles, data=_device.to_host64(forward_project_stack(p, vol.data)))

@@ -136,3 +136,36 @@ def test_device_plan_weights_match_host(tf):
     dev = p.device_tables()
     np.testing.assert_array_equal(dev["ab"].cpu().numpy(), host.ab)
     np.testing.assert_allclose(dev["wts"].cpu().numpy(), host.wts, rtol=2e-6, atol=1e-6)
+
+
+def test_type2_and_forward_project_match_reference(tf):
+    d = golden("nufft_n32_p20_nd40.npz")
+    p = _plan(tf, d["angles"], 40, 32)
+    assert rel_l2(tf.type2(p, d["img"]), d["type2"]) < 1e-5
+    proj = tf.forward_project(p, d["img"])
+    assert rel_l2(proj.data[0], d["proj"]) < 1e-5
+
+
+@pytest.mark.parametrize("n,n_ang,nd", [(33, 10, 33), (128, 60, 256), (2048, 128, 2048)])
+def test_forward_project_vs_oracle(tf, n, n_ang, nd):
+    import oracle as O
+
+    ang = np.linspace(0, np.pi, n_ang, endpoint=False)
+    img = np.random.default_rng(n).standard_normal((n, n))
+    ref = O.forward_project(O.make_plan(n, ang, nd), img)
+    got = tf.forward_project(_plan(tf, ang, nd, n), img).data[0]
+    assert rel_l2(got, ref) < 1e-5
+
+
+def test_projector_adjointness(tf):
+    """<R f, g> = <f, R* g> on the GPU pair (test_radon.py:113-120)."""
+    from paper_2603_28756_b200.radon import back_project_stack, forward_project_stack
+
+    ang = np.linspace(0, np.pi, 45, endpoint=False)
+    p = _plan(tf, ang, 96, 64)
+    rng = np.random.default_rng(9)
+    f, g = rng.standard_normal((3, 64, 64)), rng.standard_normal((3, 45, 96))
+    rf = forward_project_stack(p, f).double().cpu().numpy()
+    rtg = back_project_stack(p, g).double().cpu().numpy()
+    lhs, rhs = np.sum(rf * g), np.sum(f * rtg)
+    assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
