@@ -8,6 +8,9 @@ tensors pass through without copies and results stay on the device.
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import torch
 
@@ -67,23 +70,60 @@ def as_stack(f, what: str = "input"):
 _CHUNK_ELEMS = 1 << 25  # 256 MB of float64 per staged copy
 
 
+_STAGE_THREADS = min(8, os.cpu_count() or 1)
+_stage_pool = None
+
+
+def _pool():
+    global _stage_pool
+    if _stage_pool is None:
+        _stage_pool = ThreadPoolExecutor(max_workers=_STAGE_THREADS)
+    return _stage_pool
+
+
 def to_device(arr: np.ndarray) -> torch.Tensor:
     """float64 (or any real) host array -> contiguous fp32 device tensor.
 
-    The host array is copied as is (no host-side conversion pass) in chunks of
-    256 MB and narrowed to fp32 on the device."""
+    Large arrays go through two page-locked staging buffers (torch's caching host
+    allocator): host threads fill chunk i+1 (numpy copies release the GIL) while
+    chunk i is in flight to the device, where it is narrowed to fp32."""
     arr = np.ascontiguousarray(arr)
     dev = _lib.device()
-    if arr.dtype == np.float32:
-        return torch.from_numpy(arr).to(dev)
-    if arr.dtype != np.float64:
+    if arr.dtype not in (np.float32, np.float64):
         arr = arr.astype(np.float64)
     out = torch.empty(arr.shape, dtype=torch.float32, device=dev)
-    src = torch.from_numpy(arr).reshape(-1)
+    flat = arr.reshape(-1)
     dst = out.reshape(-1)
-    for lo in range(0, src.numel(), _CHUNK_ELEMS):
-        hi = min(src.numel(), lo + _CHUNK_ELEMS)
-        dst[lo:hi].copy_(src[lo:hi].to(dev))
+    total = flat.size
+    if total * flat.itemsize < (64 << 20):  # small: one plain copy
+        if not flat.flags.writeable:
+            flat = flat.copy()
+        dst.copy_(torch.from_numpy(flat).to(dev))
+        return out
+    chunk = _CHUNK_ELEMS
+    tdt = torch.float64 if flat.dtype == np.float64 else torch.float32
+    stages = [torch.empty(chunk, dtype=tdt, pin_memory=True) for _ in range(2)]
+    events = [None, None]
+    stream = torch.cuda.current_stream()
+
+    def fill(stage, lo, hi):
+        part = (hi - lo) // _STAGE_THREADS + 1
+        view = stage.numpy()
+        futs = [_pool().submit(np.copyto, view[a - lo:min(hi, a + part) - lo], flat[a:min(hi, a + part)])
+                for a in range(lo, hi, part)]
+        for f in futs:
+            f.result()
+
+    for i, lo in enumerate(range(0, total, chunk)):
+        hi = min(total, lo + chunk)
+        b = i % 2
+        if events[b] is not None:
+            events[b].synchronize()  # the stage's previous upload has finished reading it
+        fill(stages[b], lo, hi)
+        dev_chunk = stages[b][:hi - lo].to(dev, non_blocking=True)
+        dst[lo:hi].copy_(dev_chunk)
+        events[b] = torch.cuda.Event()
+        events[b].record(stream)
     return out
 
 

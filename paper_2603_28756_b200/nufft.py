@@ -191,7 +191,7 @@ class NufftPlan:
             samples = np.ascontiguousarray(self.sampling.samples, dtype=np.float64)
             h = self._tables or PlanTables(self.grid_side, samples, self.kernel_width,
                                            self.kernel_params, self.os_side, weights=False)
-            up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+            up = lambda a: torch.from_numpy(np.array(a, copy=True, order="C")).to(dev)  # noqa: E731
             kxy = up(samples)
             ab = torch.empty((samples.shape[0], 2), dtype=torch.int32, device=dev)
             wts = torch.empty((samples.shape[0], 2 * self.kernel_width), dtype=torch.float32,
