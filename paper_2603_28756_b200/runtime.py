@@ -151,6 +151,13 @@ class SlabComm:
         return w if self.group is None else dist.get_global_rank(self.group, w)
 
     def exchange(self, slab: torch.Tensor):
+        return self.exchange_finish(self.exchange_start(slab))
+
+    def exchange_start(self, slab: torch.Tensor):
+        """Post the boundary-plane sends/receives of ``slab``.  With NCCL and device
+        tensors the transfers run on NCCL's stream while the caller keeps
+        launching work (the solver overlaps them with the slab's Toeplitz
+        apply); ``exchange_finish`` makes the current stream wait for them."""
         part = self.part
         if slab.shape[0] != part.size:
             raise ProtocolError(f"slab has {slab.shape[0]} slices, partition owns {part.size}")
@@ -174,12 +181,20 @@ class SlabComm:
                                   self.group))
             ops.append(dist.P2POp(dist.irecv, hi, self._peer(part.upper), self.group))
             self.counts["halo"] += 1
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        if staged:  # host-staged (gloo): complete now
+            for req in reqs:
                 req.wait()
-        if staged and slab.is_cuda:
-            lo = lo.to(slab.device) if lo is not None else None
-            hi = hi.to(slab.device) if hi is not None else None
+            reqs = []
+            if slab.is_cuda:
+                lo = lo.to(slab.device) if lo is not None else None
+                hi = hi.to(slab.device) if hi is not None else None
+        return reqs, lo, hi
+
+    def exchange_finish(self, handle):
+        reqs, lo, hi = handle
+        for req in reqs:
+            req.wait()
         return lo, hi
 
     def allreduce(self, values: torch.Tensor) -> torch.Tensor:
