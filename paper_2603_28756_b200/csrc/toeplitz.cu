@@ -550,6 +550,114 @@ k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict_
   if (t == 0) bulk_wait<0>();
 }
 
+// K2, ping-pong variant: same contract as k_cols_conv_tma<..., NB = 1>.
+// * the FFT exchanges alternate between two shared buffers, so each exchange
+//   costs one CTA barrier instead of two;
+// * results go straight to global memory: 8-byte stores, 4 consecutive lanes
+//   complete one 32-byte row-block piece, addresses from a per-thread base plus
+//   a constant stride (no per-element index arithmetic);
+// * the (column, slice) walk is kept in counters -- no divisions in the loop.
+// Shared memory: S input stages + 2 exchange buffers (102 KB at M = 4096, two
+// CTAs per SM).
+template <int M, int E, int S, bool FLIP>
+__global__ void __launch_bounds__(M / E, 2)
+k_cols_conv_pp(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ PQ,
+               const float* __restrict__ Bi, int ncols, int nrb, int nslices, int boxr,
+               c32* __restrict__ T) {
+  constexpr int TT = M / E;
+  constexpr int SB = group_stride(M, 1);
+  constexpr int CL = M / 2;
+  constexpr int H = M / 2 + 1;
+  static_assert(FftShape<M, E>::NP % 2 == 1, "ping-pong needs an even exchange count");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  c32* inb = reinterpret_cast<c32*>(smem_raw);   // [S][CL]
+  c32* xbuf = inb + S * CL;                       // [2][SB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * SB);
+  uint64_t* empty = full + S;
+  const int t = threadIdx.x;
+  if ((int)blockIdx.x >= ncols) return;
+  const int my_cols = (ncols - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const long long nitems = (long long)my_cols * nslices;
+  const int nbox = (nrb + boxr - 1) / boxr;
+  const uint32_t box_bytes = (uint32_t)boxr * RB * sizeof(c32);
+  const int col_len = nrb * RB;
+  // producer walk (thread 0): item -> (column, slice), S items ahead of the consumer
+  int p_col = blockIdx.x, p_sl = 0;
+  auto issue = [&](int s) {
+    mbar_expect_tx(&full[s], nbox * box_bytes);
+    for (int q = 0; q < nbox; ++q)
+      tma_load_4d(inb + s * CL + q * boxr * RB, &tmap, 0, p_col, q * boxr, p_sl, &full[s]);
+    if (++p_sl == nslices) {
+      p_sl = 0;
+      p_col += gridDim.x;
+    }
+  };
+  if (t == 0) {
+    tma_prefetch_desc(&tmap);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TT);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int s = 0; s < S && s < nitems; ++s) issue(s);
+
+  const TwDirect twt;
+  c32 pq[E];
+  float bi[FLIP ? E : 1];
+  // consumer walk: per-thread store base of element j = t (+ 256 m) of (col, sl)
+  int c_col = blockIdx.x, c_sl = 0;
+  const long long m_stride = (long long)(TT / RB) * H * RB;  // j += TT -> 64 row blocks on
+  const long long slice_stride = (long long)nrb * H * RB;
+  const long long t_off = (long long)(t >> 2) * H * RB + (t & 3);
+  for (long long i = 0; i < nitems; ++i) {
+    const int s = (int)(i % S);
+    const uint32_t parity = (uint32_t)((i / S) & 1);
+    if (c_sl == 0) {
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        pq[m] = __ldg(PQ + (long long)c_col * M + t + TT * m);
+        if constexpr (FLIP) bi[m] = __ldg(Bi + (long long)c_col * M + t + TT * m);
+      }
+    }
+    mbar_wait(&full[s], parity);
+    c32 v[1][E];
+    const c32* in = inb + s * CL;
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+      const int j = t + TT * m;
+      v[0][m] = j < col_len ? in[j] : mk(0.f, 0.f);
+    }
+    mbar_arrive(&empty[s]);
+    fftn<M, E, false, true, false, 1, TwDirect, true>(v, xbuf, SB, t, twt);
+    if (t == 0 && i + S < nitems) {
+      mbar_wait(&empty[s], parity);
+      issue(s);
+    }
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      if constexpr (FLIP) {
+        v[0][m] = pfma(mk(v[0][m].y, v[0][m].x), mk(bi[m], bi[m]), pmul(v[0][m], pq[m]));
+      } else {
+        v[0][m] = pmul(v[0][m], pq[m]);
+      }
+    }
+    fftn<M, E, true, false, true, 1, TwDirect, true>(v, xbuf, SB, t, twt);
+    c32* dst = T + c_sl * slice_stride + (long long)c_col * RB + t_off;
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+      if (t + TT * m < col_len) dst[m * m_stride] = v[0][m];
+    }
+    if (++c_sl == nslices) {
+      c_sl = 0;
+      c_col += gridDim.x;
+    }
+  }
+}
+
 // forward-only column FFT (PSF spectra): S[z][c][kx] = FFT_ix(column c of T)
 template <int M, int E, int G>
 __global__ void __launch_bounds__(G*(M / E))
@@ -830,6 +938,31 @@ int launch_cols_conv_tma_t(c32* T, const c32* PQ, const float* Bi, int col_len,
 }
 
 template <int M, bool FLIP>
+int launch_cols_conv_pp_t(c32* T, const c32* PQ, const float* Bi, int col_len,
+                          long long nslices, cudaStream_t st) {
+  constexpr int E = eper<M>();
+  constexpr int TT = M / E;
+  const int ncols = M / 2 + 1;
+  const int nrb = nrb_of(col_len);
+  const int boxr = std::min(nrb, 256);
+  CUtensorMap map;
+  TF_TRY(encode_tmap(&map, T, M, nrb, nslices, boxr));
+  const size_t smem = sizeof(c32) * ((size_t)CONV_STAGES * (M / 2) + 2 * group_stride(M, 1)) +
+                      2 * CONV_STAGES * sizeof(uint64_t);
+  auto kern = k_cols_conv_pp<M, E, CONV_STAGES, FLIP>;
+  TF_TRY(prep_kernel(kern, smem));
+  int blocks_per_sm = 0;
+  TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, TT, smem),
+                    "occupancy"));
+  const int grid = std::max(1, std::min(ncols, std::max(1, blocks_per_sm) * num_sms()));
+  KernelTimer tm;
+  timer_begin(tm, 1, st);
+  kern<<<grid, TT, smem, st>>>(map, PQ, Bi, ncols, nrb, (int)nslices, boxr, T);
+  timer_end(tm);
+  return check_launch("k_cols_conv_pp");
+}
+
+template <int M, bool FLIP>
 int launch_cols_conv_t(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
                        cudaStream_t st) {
   constexpr int E = eper<M>(), G = cols_g<M>();
@@ -853,11 +986,11 @@ template <int M>
 int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
                      bool flip, cudaStream_t st) {
   if (2 * col_len > M) return fail_arg("k_cols_conv: column length %d exceeds M/2", col_len);
-  // tuning/debug knob: TF_K2 = generic | nb1 | nb1c | nb2 | nb2c (default nb1)
+  // tuning/debug knob: TF_K2 = pp (default) | nb1 | nb1c | nb2 | nb2c | nb1p | e8 | generic
   static const char* k2 = getenv("TF_K2");
-  static const int variant = !k2 ? 0 : !strcmp(k2, "generic") ? -1 : !strcmp(k2, "nb1") ? 0
+  static const int variant = !k2 ? 6 : !strcmp(k2, "generic") ? -1 : !strcmp(k2, "nb1") ? 0
                           : !strcmp(k2, "nb1c") ? 1 : !strcmp(k2, "nb2") ? 2 : !strcmp(k2, "nb1p") ? 4
-                          : !strcmp(k2, "e8") ? 5 : 3;
+                          : !strcmp(k2, "e8") ? 5 : !strcmp(k2, "pp") ? 6 : 3;
   if constexpr (M >= 1024 && M <= 4096) {
     switch (variant) {
       case 0: return flip ? launch_cols_conv_tma_t<M, true, 1, false>(T, PQ, Bi, col_len, nslices, st)
@@ -872,6 +1005,8 @@ int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long l
                           : launch_cols_conv_tma_t<M, false, 1, false, true>(T, PQ, Bi, col_len, nslices, st);
       case 5: return flip ? launch_cols_conv_tma_t<M, true, 1, false, false, 8>(T, PQ, Bi, col_len, nslices, st)
                           : launch_cols_conv_tma_t<M, false, 1, false, false, 8>(T, PQ, Bi, col_len, nslices, st);
+      case 6: return flip ? launch_cols_conv_pp_t<M, true>(T, PQ, Bi, col_len, nslices, st)
+                          : launch_cols_conv_pp_t<M, false>(T, PQ, Bi, col_len, nslices, st);
       default: break;
     }
   }
