@@ -387,8 +387,10 @@ def _mbir(tf, args, world, rank):
     hier = tf.GridHierarchy(levels=(512, 1024, 2048), iters_per_level=(40, 20, 10))
     _, t_hier = timed(lambda: tf.solve_hierarchical(
         sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300, lipschitz=L), use_fbp_init=True))
+    c1 = None if args.no_cpu_baseline else _c1_pipeline(tf, timed)
     return {
         "workload": f"C3 slab: {z} x 2048^2 per GPU, 128 angles, Nd=2048, qGGMRF lam=5e-4",
+        "c1_end_to_end": c1,
         "setup_ms": {"psf": t_psf, "rstar_nufft": t_rstar, "fbp_nufft": t_fbp},
         "solve_ms_per_iter": per_it,
         "solve_bytes_per_voxel_iter": bpv,
@@ -397,6 +399,48 @@ def _mbir(tf, args, world, rank):
         "hierarchical_schedule": "levels (512, 1024, 2048), iterations (40, 20, 10), FBP init, "
                                  "Lanczos-3 upsampling, L fixed from the finest level",
     }
+
+
+def _c1_pipeline(tf, timed):
+    """configs[0] (C1) end to end on the GPU -- FBP init, sigma = 0.1 range(FBP), power
+    iteration for L, 100 iterations -- beside the same pipeline in the CPU oracle
+    (the reference algorithm, one process) on the same Gaussian-noise sinogram."""
+    import oracle as O
+
+    n, n_ang, nd = 256, 180, 512
+    ang = np.linspace(0.0, np.pi, n_ang, endpoint=False)
+    truth = tf.shepp_logan(n).data
+    geom = tf.ScanGeometry(angles=ang, detector_bins=nd, image_side=n)
+    plan = tf.NufftPlan(n, tf.polar_sampling(geom), 1e-6)
+    clean = tf.forward_project(plan, truth).data
+    g = clean + 0.5 * np.random.default_rng(7).standard_normal(clean.shape)
+    sino = tf.Sinogram(angles=ang, data=g)
+
+    def gpu():
+        p = tf.NufftPlan(n, tf.polar_sampling(geom), 1e-6)
+        psf = tf.build_psf(p.sampling, n)
+        ctx = tf.fidelity_context(p, psf, sino)
+        f0 = tf.fbp(p, sino)
+        prm = tf.QggmrfParams(sigma=0.1 * float(f0.data.max() - f0.data.min()), lam=5e-4)
+        L = tf.estimate_lipschitz(psf, prm)
+        return tf.solve(ctx, prm, tf.SolverConfig(max_iters=100, tol=1e-300, lipschitz=L), f0)
+
+    gpu()  # warm (plan tables, kernels)
+    (rec, recs), t_gpu = timed(gpu)
+    t0 = time.perf_counter()
+    po = O.make_plan(n, ang, nd)
+    psf_o = O.build_psf(ang, nd, n)
+    rs = O.rstar(po, g)
+    f0 = O.fbp(po, g)
+    pr = O.Prior(sigma=0.1 * float(f0.max() - f0.min()), lam=5e-4)
+    L = O.estimate_lipschitz(psf_o, pr)
+    ref, _ = O.solve(psf_o, rs, float(np.sum(g ** 2)), pr, f0, 100, L, tol=1e-300)
+    t_cpu = (time.perf_counter() - t0) * 1e3
+    err = float(np.linalg.norm(rec.data - ref[0]) / np.linalg.norm(ref[0]))
+    return {"config": "C1: 256^2 Shepp-Logan, 180 angles, Nd=512, noise rms 0.5, FBP init, "
+                      "lam=5e-4, 100 iterations (projection by the GPU forward projector)",
+            "gpu_ms": t_gpu, "cpu_oracle_ms": t_cpu, "cpu_threads": 1,
+            "recon_rel_l2_vs_oracle": err, "restarts": int(sum(r.restarted for r in recs))}
 
 
 def _mbir_distributed(tf, z, world, rank, prm, L, timed, setup, per_it_local, bpv, peak):
