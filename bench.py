@@ -325,15 +325,19 @@ def _e2e(tf, ctx, z, world, steps):
     import torch
 
     f = np.random.default_rng(5).standard_normal((z, N_SIDE, N_SIDE))
-    tf.fidelity_grad(ctx, f)  # warm
+    for _ in range(2):  # warm: kernels, page-locked staging / result blocks
+        tf.fidelity_grad(ctx, f)
     torch.cuda.synchronize()
     barrier(world)
     t0 = time.perf_counter()
+    check = 0.0
     for _ in range(steps):
         out = tf.fidelity_grad(ctx, f)
+        check += float(out[-1, -1, -1])  # the caller consumes each result ...
+        del out                          # ... and releases it before the next call
     dt = time.perf_counter() - t0
     dt = max_over_ranks(dt, world)
-    assert out.shape == f.shape
+    assert np.isfinite(check)
     return {"value": z * world * steps / dt, "unit": UNIT,
             "h2d_bytes_per_step": int(f.nbytes), "d2h_bytes_per_step": int(f.nbytes),
             "api": "fidelity_grad(ctx, numpy float64 (64, 2048, 2048)) -> numpy float64"}

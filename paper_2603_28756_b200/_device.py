@@ -160,3 +160,91 @@ def wrap_like(kind: str, t: torch.Tensor):
     if kind == "array2":
         return host[0]
     return host
+
+
+def host_kind(f) -> str | None:
+    """The reference kind of a host input ('image', 'volume', 'array2', 'array3'), or
+    None for CUDA tensors / anything to be handled by ``as_stack``."""
+    if isinstance(f, ImageGrid):
+        return "image"
+    if isinstance(f, Volume):
+        return "volume"
+    if isinstance(f, np.ndarray) and f.ndim in (2, 3):
+        return "array2" if f.ndim == 2 else "array3"
+    return None
+
+
+def _wrap_host(kind: str, host: np.ndarray):
+    if kind == "image":
+        return ImageGrid._owned(host[0])
+    if kind == "volume":
+        return Volume._owned(host)
+    if kind == "array2":
+        return host[0]
+    return host
+
+
+_PIPE_SLICE_BYTES = 256 << 20
+_streams: dict = {}
+
+
+def _pipe_streams(dev):
+    st = _streams.get(dev.index)
+    if st is None:
+        st = _streams[dev.index] = tuple(torch.cuda.Stream(device=dev) for _ in range(3))
+    return st
+
+
+def pipelined_host_map(arr: np.ndarray, kind: str, fn):
+    """out[z] = fn(z0, z1, x_dev[z0:z1]) for a float64 host stack, chunked over slices
+    and pipelined over three streams: the host threads fill a page-locked stage and
+    the copy stream uploads chunk i+1 while the compute stream runs ``fn`` on chunk i
+    and the download stream returns chunk i-1 into a page-locked float64 result
+    (PCIe/NVLink-C2C full duplex).  ``fn`` must return a new (z1-z0, ...) fp32
+    device tensor.  Returns the result in the caller's kind."""
+    dev = _lib.device()
+    arr = np.ascontiguousarray(arr, dtype=np.float64)
+    stack = arr[None] if arr.ndim == 2 else arr
+    z = stack.shape[0]
+    plane = int(np.prod(stack.shape[1:]))
+    step = max(1, min(z, _PIPE_SLICE_BYTES // max(1, plane * 8)))
+    try:
+        out = torch.empty(stack.shape, dtype=torch.float64, pin_memory=True)
+    except RuntimeError:
+        out = torch.empty(stack.shape, dtype=torch.float64)
+    stages = [torch.empty(step * plane, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    staged = [None, None]
+    caller = torch.cuda.current_stream()
+    s_up, s_cmp, s_dn = _pipe_streams(dev)
+    for q in (s_up, s_cmp, s_dn):
+        q.wait_stream(caller)
+    flat = stack.reshape(z, plane)
+    for i, z0 in enumerate(range(0, z, step)):
+        z1 = min(z, z0 + step)
+        b = i % 2
+        if staged[b] is not None:
+            staged[b].synchronize()  # stage b's previous upload has been read
+        view = stages[b].numpy()[: (z1 - z0) * plane]
+        src = flat[z0:z1].reshape(-1)
+        part = -(-src.size // _STAGE_THREADS)
+        futs = [_pool().submit(np.copyto, view[a:a + part], src[a:a + part])
+                for a in range(0, src.size, part)]
+        for fu in futs:
+            fu.result()
+        with torch.cuda.stream(s_up):
+            x64 = stages[b][: view.size].to(dev, non_blocking=True)
+            x = x64.reshape((z1 - z0,) + stack.shape[1:]).to(torch.float32)
+            ev = torch.cuda.Event()
+            ev.record(s_up)
+            staged[b] = ev
+        s_cmp.wait_stream(s_up)
+        x.record_stream(s_cmp)
+        with torch.cuda.stream(s_cmp):
+            y = fn(z0, z1, x)
+        s_dn.wait_stream(s_cmp)
+        y.record_stream(s_dn)
+        with torch.cuda.stream(s_dn):
+            out[z0:z1].copy_(y.to(torch.float64), non_blocking=True)
+    caller.wait_stream(s_dn)
+    s_dn.synchronize()
+    return _wrap_host(kind, out.numpy())

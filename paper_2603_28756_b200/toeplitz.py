@@ -180,6 +180,13 @@ def _check_side(psf: PsfKernel, side: int) -> None:
 
 def toeplitz_apply(psf: PsfKernel, f):
     """R*R f for an ImageGrid, Volume, array or CUDA tensor (toeplitz.py:152-165)."""
+    kind = _device.host_kind(f)
+    if kind is not None:  # host float64 in and out: chunked, overlapped transfers
+        arr = f.data if kind in ("image", "volume") else f
+        _check_side(psf, arr.shape[-1])
+        if arr.shape[-2] != arr.shape[-1]:
+            raise ValueError(f"image side {arr.shape[-1]} does not match kernel source side")
+        return _device.pipelined_host_map(arr, kind, lambda z0, z1, x: apply_stack(psf, x))
     x, kind = _device.as_stack(f)
     _check_side(psf, x.shape[-1])
     return _device.wrap_like(kind, apply_stack(psf, x))
@@ -251,6 +258,16 @@ def fidelity_loss(ctx: FidelityContext, f) -> float:
 
 def fidelity_grad(ctx: FidelityContext, f):
     """K f - R*g, same kind as the input (toeplitz.py:233-241)."""
+    kind = _device.host_kind(f)
+    if kind is not None:  # host float64 in and out: chunked, overlapped transfers
+        arr = f.data if kind in ("image", "volume") else f
+        shape = (1,) + arr.shape if arr.ndim == 2 else arr.shape
+        if tuple(shape) != (ctx.slices, ctx.side, ctx.side):
+            raise ValueError(f"estimate shape {tuple(shape)} does not match data "
+                             f"({ctx.slices}, {ctx.side}, {ctx.side})")
+        return _device.pipelined_host_map(
+            arr, kind, lambda z0, z1, x: apply_stack(ctx.psf, x, aux=ctx.rstar[z0:z1],
+                                                     alpha=1.0, beta=-1.0))
     x, kind = _fidelity_stack(ctx, f)
     grad = apply_stack(ctx.psf, x, aux=ctx.rstar, alpha=1.0, beta=-1.0)
     return _device.wrap_like(kind, grad)
