@@ -5,7 +5,7 @@ TAG=${1:-r01}
 mkdir -p gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-mbir > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_rows|k_cols' -s 6 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_rows|k_cols_conv' -s 6 -c 3 \
   -o gpurun_out/prof_toeplitz_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-mbir > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_prior|k_energy' -c 2 \
   -o gpurun_out/prof_solver_$TAG -f python tools/solver_probe.py > /dev/null 2>&1
