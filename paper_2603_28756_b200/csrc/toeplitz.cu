@@ -937,7 +937,7 @@ int launch_cols_conv_tma_t(c32* T, const c32* PQ, const float* Bi, int col_len,
   return check_launch("k_cols_conv_tma");
 }
 
-template <int M, bool FLIP>
+template <int M, bool FLIP, int NS = CONV_STAGES>
 int launch_cols_conv_pp_t(c32* T, const c32* PQ, const float* Bi, int col_len,
                           long long nslices, cudaStream_t st) {
   constexpr int E = eper<M>();
@@ -947,9 +947,9 @@ int launch_cols_conv_pp_t(c32* T, const c32* PQ, const float* Bi, int col_len,
   const int boxr = std::min(nrb, 256);
   CUtensorMap map;
   TF_TRY(encode_tmap(&map, T, M, nrb, nslices, boxr));
-  const size_t smem = sizeof(c32) * ((size_t)CONV_STAGES * (M / 2) + 2 * group_stride(M, 1)) +
-                      2 * CONV_STAGES * sizeof(uint64_t);
-  auto kern = k_cols_conv_pp<M, E, CONV_STAGES, FLIP>;
+  const size_t smem = sizeof(c32) * ((size_t)NS * (M / 2) + 2 * group_stride(M, 1)) +
+                      2 * NS * sizeof(uint64_t);
+  auto kern = k_cols_conv_pp<M, E, NS, FLIP>;
   TF_TRY(prep_kernel(kern, smem));
   int blocks_per_sm = 0;
   TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, TT, smem),
@@ -990,7 +990,7 @@ int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long l
   static const char* k2 = getenv("TF_K2");
   static const int variant = !k2 ? 6 : !strcmp(k2, "generic") ? -1 : !strcmp(k2, "nb1") ? 0
                           : !strcmp(k2, "nb1c") ? 1 : !strcmp(k2, "nb2") ? 2 : !strcmp(k2, "nb1p") ? 4
-                          : !strcmp(k2, "e8") ? 5 : !strcmp(k2, "pp") ? 6 : 3;
+                          : !strcmp(k2, "e8") ? 5 : !strcmp(k2, "pp") ? 6 : !strcmp(k2, "pp1") ? 7 : 3;
   if constexpr (M >= 1024 && M <= 4096) {
     switch (variant) {
       case 0: return flip ? launch_cols_conv_tma_t<M, true, 1, false>(T, PQ, Bi, col_len, nslices, st)
@@ -1007,6 +1007,8 @@ int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long l
                           : launch_cols_conv_tma_t<M, false, 1, false, false, 8>(T, PQ, Bi, col_len, nslices, st);
       case 6: return flip ? launch_cols_conv_pp_t<M, true>(T, PQ, Bi, col_len, nslices, st)
                           : launch_cols_conv_pp_t<M, false>(T, PQ, Bi, col_len, nslices, st);
+      case 7: return flip ? launch_cols_conv_pp_t<M, true, 1>(T, PQ, Bi, col_len, nslices, st)
+                          : launch_cols_conv_pp_t<M, false, 1>(T, PQ, Bi, col_len, nslices, st);
       default: break;
     }
   }
