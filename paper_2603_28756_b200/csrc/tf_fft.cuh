@@ -299,19 +299,33 @@ __device__ __forceinline__ void load_canonical(c32 (&v)[NB][E], const c32* sm, i
     for (int b = 0; b < NB; ++b) v[b][m] = sm[b * sbs + canon_word<M, E>(t, m)];
 }
 
+// Pass P with its twiddles already in `tw` (null for P = 0).  The twiddles of
+// pass P+1 are fetched *before* the exchange that precedes it, so their loads
+// (or product-tree FMAs) overlap the shared-memory round trip and the barrier
+// instead of stalling the next pass (TF_TW_EARLY = 0 restores in-place fetches).
+#ifndef TF_TW_EARLY
+#define TF_TW_EARLY 1
+#endif
 template <int M, int E, int P, bool INV, bool ZIN, bool HOUT, int NB, bool PP, typename TwF>
 __device__ __forceinline__ void fft_passes_from(c32 (&v)[NB][E], c32* sm, int sbs, int t,
-                                                const TwF& twf) {
+                                                const TwF& twf,
+                                                const PassTw<M, E, P>* tw = nullptr) {
   using S = FftShape<M, E>;
   constexpr bool LAST = P + 1 == S::NP;
   if constexpr (P > 0) {
-    PassTw<M, E, P> tw;
-    twf(tw, t);
-    fft_pass<M, E, P, INV, false, HOUT && LAST, NB>(v, &tw);
+    if constexpr (TF_TW_EARLY) {
+      fft_pass<M, E, P, INV, false, HOUT && LAST, NB>(v, tw);
+    } else {
+      PassTw<M, E, P> own;
+      twf(own, t);
+      fft_pass<M, E, P, INV, false, HOUT && LAST, NB>(v, &own);
+    }
   } else {
     fft_pass<M, E, P, INV, ZIN, HOUT && LAST, NB>(v, (const PassTw<M, E, P>*)nullptr);
   }
   if constexpr (!LAST) {
+    PassTw<M, E, P + 1> next;
+    if constexpr (TF_TW_EARLY) twf(next, t);
     // ping-pong: exchange P uses buffer half P % 2, so the next exchange's stores
     // cannot overwrite words still being read and the trailing barrier goes away
     c32* buf = (PP && (P & 1)) ? sm + NB * sbs : sm;
@@ -319,7 +333,7 @@ __device__ __forceinline__ void fft_passes_from(c32 (&v)[NB][E], c32* sm, int sb
     __syncthreads();
     load_canonical<M, E, NB>(v, buf, sbs, t);
     if constexpr (!PP) __syncthreads();
-    fft_passes_from<M, E, P + 1, INV, ZIN, HOUT, NB, PP>(v, sm, sbs, t, twf);
+    fft_passes_from<M, E, P + 1, INV, ZIN, HOUT, NB, PP>(v, sm, sbs, t, twf, &next);
   }
 }
 
