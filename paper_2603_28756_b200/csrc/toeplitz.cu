@@ -550,6 +550,16 @@ k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict_
   if (t == 0) bulk_wait<0>();
 }
 
+// twiddle source of the ping-pong column kernel (tuning: TF_K2_TWDIRECT=0 -> product tree)
+#ifndef TF_K2_TWDIRECT
+#define TF_K2_TWDIRECT 0
+#endif
+#if TF_K2_TWDIRECT
+using K2Tw = TwDirect;
+#else
+using K2Tw = TwTable;
+#endif
+
 // K2, ping-pong variant: same contract as k_cols_conv_tma<..., NB = 1>.
 // * the FFT exchanges alternate between two shared buffers, so each exchange
 //   costs one CTA barrier instead of two;
@@ -605,7 +615,7 @@ k_cols_conv_pp(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__
   if (t == 0)
     for (int s = 0; s < S && s < nitems; ++s) issue(s);
 
-  const TwDirect twt;
+  const K2Tw twt;
   c32 pq[E];
   float bi[FLIP ? E : 1];
   // consumer walk: per-thread store base of element j = t (+ 256 m) of (col, sl)
@@ -632,7 +642,7 @@ k_cols_conv_pp(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__
       v[0][m] = j < col_len ? in[j] : mk(0.f, 0.f);
     }
     mbar_arrive(&empty[s]);
-    fftn<M, E, false, true, false, 1, TwDirect, true>(v, xbuf, SB, t, twt);
+    fftn<M, E, false, true, false, 1, K2Tw, true>(v, xbuf, SB, t, twt);
     if (t == 0 && i + S < nitems) {
       mbar_wait(&empty[s], parity);
       issue(s);
@@ -645,7 +655,7 @@ k_cols_conv_pp(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__
         v[0][m] = pmul(v[0][m], pq[m]);
       }
     }
-    fftn<M, E, true, false, true, 1, TwDirect, true>(v, xbuf, SB, t, twt);
+    fftn<M, E, true, false, true, 1, K2Tw, true>(v, xbuf, SB, t, twt);
     c32* dst = T + c_sl * slice_stride + (long long)c_col * RB + t_off;
 #pragma unroll
     for (int m = 0; m < E / 2; ++m) {
