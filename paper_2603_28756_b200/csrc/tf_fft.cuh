@@ -238,6 +238,17 @@ struct TwTable {
   }
 };
 
+// small [r][k] power tables where NS <= 16 (L1-resident, 2 KB), product tree for
+// the per-thread last-pass powers (whose 30 KB table would live in L2)
+struct TwMixed {
+  template <int M, int E, int P>
+  __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
+    using PT = PassTw<M, E, P>;
+    if constexpr (PT::R == 16 && PT::NS >= 2 && PT::NS <= 16) tw.from_table_direct(t);
+    else tw.from_table(t);
+  }
+};
+
 // direct power tables (see PassTw::from_table_direct)
 struct TwDirect {
   template <int M, int E, int P>

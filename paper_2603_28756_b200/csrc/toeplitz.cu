@@ -554,8 +554,10 @@ k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict_
 #ifndef TF_K2_TWDIRECT
 #define TF_K2_TWDIRECT 0
 #endif
-#if TF_K2_TWDIRECT
+#if TF_K2_TWDIRECT == 1
 using K2Tw = TwDirect;
+#elif TF_K2_TWDIRECT == 2
+using K2Tw = TwMixed;
 #else
 using K2Tw = TwTable;
 #endif
