@@ -150,6 +150,12 @@ int tf_nufft_type2(const float* d_image, long long nslices, int n, int os, int w
                    const float* d_deapod, const void* d_factor, long long n_samples, void* d_out,
                    void* d_ws, long long ws_bytes, void* stream);
 
+/* Brute-force type-2 sum in fp64 (the oracle nufft.direct_dft, nufft.py:230-249):
+ * d_out[m] (complex128) = sum_{ix,iy} d_image[ix][iy] exp(-i (kx x + ky y)) with
+ * x = ix - (n-1)/2, (kx, ky) = d_kxy[m] (fp64 [S][2]); d_image fp64 [n][n]. */
+int tf_direct_dft(const double* d_image, int n, const double* d_kxy, long long n_samples,
+                  void* d_out, void* stream);
+
 /* Real parts of the inverse DFTs of nrows complex rows given in signed-frequency
  * order (the ifftshift + ifft of radon.forward_project, radon.py:91-96), times
  * scale: d_out fp32 [nrows][nd]. */

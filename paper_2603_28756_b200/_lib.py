@@ -59,6 +59,7 @@ _SIGNATURES = {
     "tf_nufft_type2": (_c_int, [_c_void_p, _c_ll, _c_int, _c_int, _c_int] + [_c_void_p] * 5
                        + [_c_ll, _c_void_p, _c_void_p, _c_ll, _c_void_p]),
     "tf_detector_rows_inv": (_c_int, [_c_void_p, _c_ll, _c_int, _c_float, _c_void_p, _c_void_p]),
+    "tf_direct_dft": (_c_int, [_c_void_p, _c_int, _c_void_p, _c_ll, _c_void_p, _c_void_p]),
     "tf_resample_axis": (_c_int, [_c_void_p, _c_void_p, _c_ll, _c_int, _c_int, _c_ll, _c_void_p,
                                   _c_void_p, _c_int, _c_void_p]),
     "tf_timing_enable": (_c_int, [_c_int]),

@@ -116,6 +116,8 @@ int energy_fid(const float* fn, const float* fn_hi, const float* f, const float*
 int dot2(const float* x, const float* a, const float* b, long long n, double* out, double* ws,
          cudaStream_t st);
 size_t nufft_workspace_bytes(int os, long long nslices);
+int direct_dft(const double* img, int n, const double* kxy, long long S, void* out,
+               cudaStream_t st);
 size_t type2_workspace_bytes(int n, int os, long long nslices);
 int nufft_type2(const float* img, long long nslices, int n, int os, int w, const void* ab,
                 const float* wts, const void* preph, const float* deapod, const void* factor,
@@ -301,6 +303,14 @@ int tf_detector_rows_inv(const void* d_samples, long long nrows, int nd, float s
   TF_TRY(ensure_init());
   if (nrows < 0 || (nrows > 0 && (!d_samples || !d_out))) return fail_arg("bad arguments");
   return detector_rows_inv(d_samples, nrows, nd, scale, d_out, (cudaStream_t)stream);
+}
+
+int tf_direct_dft(const double* d_image, int n, const double* d_kxy, long long n_samples,
+                  void* d_out, void* stream) {
+  TF_TRY(ensure_init());
+  if (n < 1 || n_samples < 0) return fail_arg("bad direct DFT shape");
+  if (n_samples > 0 && (!d_image || !d_kxy || !d_out)) return fail_arg("null pointer");
+  return direct_dft(d_image, n, d_kxy, n_samples, d_out, (cudaStream_t)stream);
 }
 
 int tf_resample_axis(const float* d_in, float* d_out, long long outer, int n_src, int n_tgt,

@@ -432,6 +432,38 @@ __global__ void k_detector_rows_inv(const c32* __restrict__ c, int nd, int L, in
   for (int k = threadIdx.x; k < nd; k += blockDim.x) o[k] = X[k].x * g;
 }
 
+// ============================================================ direct DFT (fp64)
+// c_m = sum_{ix, iy} f[ix][iy] exp(-i (kx_m x + ky_m y)), x = ix - (N-1)/2: the
+// brute-force type-2 oracle of nufft.direct_dft (nufft.py:230-249), one thread
+// per sample, fp64 throughout (sincos per term; N <= 128 as in the reference).
+__global__ void k_direct_dft(const double* __restrict__ img, int n, const double* __restrict__ kxy,
+                             long long S, double2* __restrict__ out) {
+  const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (m >= S) return;
+  const double kx = kxy[2 * m], ky = kxy[2 * m + 1];
+  const double c0 = 0.5 * (n - 1);
+  double re = 0.0, im = 0.0;
+  for (int ix = 0; ix < n; ++ix) {
+    const double px = kx * (ix - c0);
+    for (int iy = 0; iy < n; ++iy) {
+      double sn, cs;
+      sincos(px + ky * (iy - c0), &sn, &cs);
+      const double f = __ldg(img + (long long)ix * n + iy);
+      re = fma(f, cs, re);
+      im = fma(-f, sn, im);
+    }
+  }
+  out[m] = make_double2(re, im);
+}
+
+int direct_dft(const double* img, int n, const double* kxy, long long S, void* out,
+               cudaStream_t st) {
+  if (S <= 0) return TF_OK;
+  k_direct_dft<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(img, n, kxy, S,
+                                                             reinterpret_cast<double2*>(out));
+  return check_launch("k_direct_dft");
+}
+
 // ============================================================ host dispatch
 namespace {
 

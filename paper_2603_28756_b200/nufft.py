@@ -23,6 +23,7 @@ tables are built once per (plan, device) on the host in float64:
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -31,6 +32,7 @@ from . import _device, _lib
 from .geometry import ImageGrid, PolarSampling
 
 __all__ = [
+    "SpreadKernel",
     "NufftPlan",
     "plan",
     "type1",
@@ -66,6 +68,41 @@ def _kb(x: np.ndarray, width: int, beta: float) -> np.ndarray:
     """I0(beta sqrt(1 - (2x/w)^2)) on |x| <= w/2, else 0 (nufft.py:80-87, exact)."""
     arg = 1.0 - (2.0 * np.asarray(x, dtype=np.float64) / width) ** 2
     return np.where(arg >= 0.0, np.i0(beta * np.sqrt(np.maximum(arg, 0.0))), 0.0)
+
+
+TABLE_SAMPLES_PER_UNIT = 16384
+
+
+@dataclass(frozen=True)
+class SpreadKernel:
+    """Tabulated Kaiser-Bessel kernel on |x| <= width/2 (nufft.py:60-87).
+
+    Kept for API compatibility (``NufftPlan.kernel``); the GPU plan evaluates
+    the same kernel exactly in fp64 (k_plan_weights) instead of interpolating."""
+
+    width: int
+    beta: float
+    lookup: np.ndarray = field(repr=False)
+    step: float
+
+    def __call__(self, x: np.ndarray) -> np.ndarray:
+        t = np.abs(x) / self.step
+        idx = t.astype(np.int64)
+        inside = idx < self.lookup.size - 1
+        idx = np.where(inside, idx, 0)
+        frac = t - idx
+        vals = self.lookup[idx] * (1.0 - frac) + self.lookup[idx + 1] * frac
+        return np.where(inside, vals, 0.0)
+
+
+def _build_kernel(width: int, beta: float) -> SpreadKernel:
+    """nufft.py:80-87"""
+    n_tab = int(width / 2 * TABLE_SAMPLES_PER_UNIT) + 2
+    step = (width / 2) / (n_tab - 2)
+    x = np.arange(n_tab) * step
+    table = _kb(x, width, beta)
+    table.setflags(write=False)
+    return SpreadKernel(width=width, beta=beta, lookup=table, step=step)
 
 
 def gpu_grid_side(os_side: int) -> int:
@@ -154,6 +191,7 @@ class NufftPlan:
         self.kernel_width = kernel_width_for_tolerance(tolerance)
         gamma = _BETA_SCALE.get(self.kernel_width, _BETA_SCALE_DEFAULT)
         self.kernel_params = gamma * np.pi * self.kernel_width * (1.0 - 1.0 / (2.0 * oversampling))
+        self._kernel = None
         os_side = int(np.ceil(oversampling * self.grid_side))
         if os_side % 2:
             os_side += 1
@@ -171,6 +209,13 @@ class NufftPlan:
     @property
     def sample_count(self) -> int:
         return self.sampling.count
+
+    @property
+    def kernel(self) -> SpreadKernel:
+        """The reference's tabulated spreading kernel (built on first use)."""
+        if self._kernel is None:
+            self._kernel = _build_kernel(self.kernel_width, self.kernel_params)
+        return self._kernel
 
     @property
     def tables(self) -> PlanTables:
@@ -321,3 +366,26 @@ def type2(p: NufftPlan, image) -> np.ndarray:
         raise ValueError(f"image shape {arr.shape} does not match plan grid {n}x{n}")
     out = type2_stack(p, _device.to_device(np.asarray(arr, dtype=np.float64)[None]))
     return out[0].cpu().numpy().astype(np.complex128)
+
+
+_DIRECT_MAX_SIDE = 128
+
+
+def direct_dft(sampling: PolarSampling, image) -> np.ndarray:
+    """Brute-force type-2 sum in fp64 on the GPU; the reference's accuracy oracle for
+    N <= 128 (nufft.py:230-249)."""
+    arr = image.data if isinstance(image, ImageGrid) else np.asarray(image)
+    n = arr.shape[0]
+    if arr.shape != (n, n):
+        raise ValueError("direct_dft needs a square image")
+    if n > _DIRECT_MAX_SIDE:
+        raise ValueError(f"direct_dft is an oracle for N <= {_DIRECT_MAX_SIDE}, got N={n}")
+    lib = _lib.ensure_ready()
+    dev = _lib.device()
+    img = torch.from_numpy(np.array(arr, dtype=np.float64, order="C")).to(dev)
+    kxy = torch.from_numpy(np.array(sampling.samples, dtype=np.float64, order="C")).to(dev)
+    out = torch.empty((sampling.count, 2), dtype=torch.float64, device=dev)
+    _lib.check(lib.tf_direct_dft(img.data_ptr(), n, kxy.data_ptr(), sampling.count,
+                                 out.data_ptr(), _lib.stream_handle()), "tf_direct_dft")
+    o = out.cpu().numpy()
+    return o[:, 0] + 1j * o[:, 1]

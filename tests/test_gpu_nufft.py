@@ -169,3 +169,15 @@ def test_projector_adjointness(tf):
     rtg = back_project_stack(p, g).double().cpu().numpy()
     lhs, rhs = np.sum(rf * g), np.sum(f * rtg)
     assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+
+
+def test_direct_dft_matches_reference_type2(tf):
+    """The fp64 brute-force sum agrees with the reference's type2 to its tolerance
+    (test_nufft.py:70-85) and with our type2."""
+    d = golden("nufft_n32_p20_nd40.npz")
+    p = _plan(tf, d["angles"], 40, 32)
+    direct = tf.direct_dft(p.sampling, d["img"])
+    assert rel_l2(d["type2"], direct) < 1e-6
+    assert rel_l2(tf.type2(p, d["img"]), direct) < 1e-5
+    with pytest.raises(ValueError):
+        tf.direct_dft(p.sampling, np.zeros((130, 130)))

@@ -130,3 +130,15 @@ def test_plan_validation():
     p = NufftPlan(16, s, 1e-6)
     assert p.kernel_width == 7 and p.os_side == 32 and p.gpu_side == 32
     assert NufftPlan(200, s, 1e-6).gpu_side == 512
+
+
+def test_spread_kernel_table():
+    """nufft.py:60-87: tabulated I0 kernel, exact at table nodes, zero off support."""
+    _, p = _plan(16, 4, 16)
+    k = p.kernel
+    assert k.width == 7 and k(np.array([0.0]))[0] == pytest.approx(np.i0(p.kernel_params))
+    assert k(np.array([3.6]))[0] == 0.0
+    x = np.linspace(-3.4, 3.4, 41)
+    beta, w = p.kernel_params, 7
+    exact = np.i0(beta * np.sqrt(1 - (2 * x / w) ** 2))
+    np.testing.assert_allclose(k(x), exact, rtol=1e-6)  # linear interpolation of the table
