@@ -37,6 +37,7 @@ __all__ = [
     "plan",
     "type1",
     "type2",
+    "direct_dft",
     "kernel_width_for_tolerance",
     "kaiser_bessel_fourier",
 ]
