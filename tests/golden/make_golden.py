@@ -12,6 +12,7 @@ which run on a GPU box where /root/reference does not exist).
 
 from __future__ import annotations
 
+import json
 import os
 import sys
 from pathlib import Path
@@ -209,9 +210,47 @@ def c2_reduced():
     print("c2_reduced.npz written")
 
 
+def fileio_fixtures():
+    """Files written by the reference's fileio (tests/golden/fileio/): raw arrays with
+    sidecars, a plan and its parse, a convergence CSV and a PGM preview."""
+    sys.path.insert(0, str(REF))
+    import dataclasses
+
+    import tomoforge as tf
+    from tomoforge import fileio
+    from tomoforge.solver import IterationRecord
+
+    out = OUT / "fileio"
+    out.mkdir(exist_ok=True)
+    rng = np.random.default_rng(31)
+    fileio.save_array(out / "vol.raw", tf.Volume(rng.standard_normal((3, 5, 5)), pixel_size=0.5))
+    fileio.save_array(out / "img.raw", tf.ImageGrid(rng.standard_normal((4, 4))))
+    fileio.save_array(out / "sino.raw", tf.Sinogram(angles=np.linspace(0, np.pi, 6, endpoint=False),
+                                                    data=rng.standard_normal((2, 6, 7))))
+    (out / "plan.toml").write_text(
+        "[geometry]\nimage_side = 64\n\n[qggmrf]\nsigma = \"auto\"\nlambda = 0.0005\np = 1.9\n\n"
+        "[solver]\nmax_iters = 40\ntol = 1e-300\nlipschitz = 1234.5\nnonneg = true\n\n"
+        "[hierarchy]\nlevels = 2\niters_per_level = [20, 10]\n\n[runtime]\nworkers = 2\nseed = 7\n\n"
+        "[files]\ninit_volume = \"vol.raw\"\n")
+    plan = fileio.load_plan(out / "plan.toml")
+    fields = {k: (str(v) if isinstance(v, Path) else v) for k, v in dataclasses.asdict(plan).items()}
+    fields["init_volume"] = Path(fields["init_volume"]).name
+    (out / "plan_parsed.json").write_text(json.dumps(fields, indent=1, default=str))
+    recs = [IterationRecord(i, 100.0 / (i + 1), 90.0 / (i + 1), 1.0 / 3, 0.5 ** i, 0.01 * i, i == 2)
+            for i in range(4)]
+    fileio.write_convergence_csv(out / "conv.csv", [(r, i % 2, 1) for i, r in enumerate(recs)],
+                                 {"seed": 7, "image_side": 64, "init": "fbp"})
+    img = tf.ImageGrid(np.outer(np.arange(6.0), np.ones(6)))
+    fileio.export_slice(out / "prev.pgm", img)
+    print("fileio fixtures written")
+
+
 if __name__ == "__main__":
     if "--only-c2" in sys.argv:
         c2_reduced()
+    elif "--only-fileio" in sys.argv:
+        fileio_fixtures()
     else:
         main()
         c2_reduced()
+        fileio_fixtures()
