@@ -265,14 +265,24 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
       }
       if (THREE_D) {
         // planes z-1 and z+1: same (dy, dx) paired across the two planes
-        const float lo_ok = (z > 0 || FP.lo != nullptr) ? 1.f : 0.f;
-        const float hi_ok = (z + 1 < nz || FP.hi != nullptr) ? 1.f : 0.f;
+        const bool lo_ok = z > 0 || FP.lo != nullptr;
+        const bool hi_ok = z + 1 < nz || FP.hi != nullptr;
+        if (lo_ok && hi_ok) {  // interior plane (uniform branch): both planes valid
 #pragma unroll
-        for (int j = 0; j < 9; ++j) {
-          const float a = ys[sm][ty + j / 3][tx + j % 3];
-          const float b = ys[sp][ty + j / 3][tx + j % 3];
-          const float2 g = drho2<P2>(mk(yv - a, yv - b), pc);
-          acc = pfma(mk(ipw.wz[j] * lo_ok, ipw.wz[j] * hi_ok), g, acc);
+          for (int j = 0; j < 9; ++j) {
+            const float a = ys[sm][ty + j / 3][tx + j % 3];
+            const float b = ys[sp][ty + j / 3][tx + j % 3];
+            acc = pfma(mk(ipw.wz[j], ipw.wz[j]), drho2<P2>(mk(yv - a, yv - b), pc), acc);
+          }
+        } else {
+          const float lo_w = lo_ok ? 1.f : 0.f, hi_w = hi_ok ? 1.f : 0.f;
+#pragma unroll
+          for (int j = 0; j < 9; ++j) {
+            const float a = ys[sm][ty + j / 3][tx + j % 3];
+            const float b = ys[sp][ty + j / 3][tx + j % 3];
+            const float2 g = drho2<P2>(mk(yv - a, yv - b), pc);
+            acc = pfma(mk(ipw.wz[j] * lo_w, ipw.wz[j] * hi_w), g, acc);
+          }
         }
       }
       const long long o = z * nn + (long long)ix * w + iy;
