@@ -378,8 +378,9 @@ k_energy_fid(Planes FN, const float* __restrict__ f, const float* __restrict__ K
     __syncthreads();
     if (inside) {
       if (with_prior) fnv = xs[s0][ty + 1][tx + 1];
-      if (Kfn) fid = fma((double)fnv, (double)fmaf(0.5f, kfn, -rs), fid);
-      if (f && Kfn) dfid = fma((double)(fnv - fv), (double)(fmaf(0.5f, kfn + kf, 0.f) - rs), dfid);
+      // fp32 products (one rounding, like the fp32 operands), fp64 running sums
+      if (Kfn) fid += (double)(fnv * fmaf(0.5f, kfn, -rs));
+      if (f && Kfn) dfid += (double)((fnv - fv) * (fmaf(0.5f, kfn + kf, 0.f) - rs));
       if (with_prior) {
         const float xv = fnv;
         // half stencil in the plane: (0,0,1), (0,1,-1), (0,1,0), (0,1,1) as two pairs
