@@ -285,6 +285,9 @@ def run_ours(args, world, rank, local):
         "frac": per_kernel[dom]["frac"], "peak_source": peak["source"],
         "traffic": _ncu_traffic(dom),
         "per_kernel": per_kernel,
+        "limiter_note": "k_cols_conv is FP32-FMA-pipe bound (ncu: FMA pipe ~67 %, top stall "
+                        "math-pipe throttle; DRAM bytes equal the algorithmic bytes); see "
+                        "DESIGN.md §3 and profiles/r01_ncu_kernels.txt",
         "gradient_total": {"bytes_per_eval": total_bytes / z,
                            "achieved": total_bytes / (tot_ms / 1e3) / 1e9,
                            "frac": total_bytes / (tot_ms / 1e3) / 1e9 / peak["value"]},
