@@ -303,6 +303,246 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
   if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = r;
 }
 
+// ============================================================ K4, symmetric pairs (3-D)
+// rho' is odd, so the 26-neighbour gradient needs each clique once:
+//   grad_prior(p) = sum_k w_k(p, p+o_k) G_k(p) - sum_k w_k(p-o_k, p) G_k(p - o_k),
+//   G_k(q) = rho'(y_q - y_{q+o_k}),
+// over the 13 offsets o_k of the half stencil (4 in the plane, 9 towards z+1);
+// w is the clique weight times [both voxels in the slice].  Per plane step a
+// thread evaluates the 13 G of its own voxel (forward terms, summed in
+// registers) and 1-2 of the 340 "strip" G on the tile's one-voxel ring that
+// are backward terms of tile voxels; all go to shared memory unweighted, and
+// after a barrier each voxel adds its 13 weighted backward terms.  The z+1
+// cliques of plane z are the backward terms of plane z+1, so they are kept one
+// step (double buffer); with a slab halo below, a pre-step at z = -1 produces
+// the cliques between the halo plane and plane 0.  Half the log2/exp2 work of
+// k_prior_update, for ~30 more shared-memory accesses per voxel.  Tiles whose
+// ring lies inside the slice (all but the outermost) take weights straight from
+// the constant bank; edge tiles derive them from four neighbour bits.
+struct HalfStencil {
+  // (dy, dx): (0,1) (1,-1) (1,0) (1,1) in the plane, then (-1..1, -1..1) towards z+1
+  __host__ __device__ static constexpr int dy(int k) { return k == 0 ? 0 : k < 4 ? 1 : (k - 4) / 3 - 1; }
+  __host__ __device__ static constexpr int dx(int k) { return k == 0 ? 1 : k < 4 ? k - 2 : (k - 4) % 3 - 1; }
+  // weight class: number of nonzero components of (dz, dy, dx)
+  __host__ __device__ static constexpr int cls(int k) { return (k >= 4) + (dy(k) != 0) + (dx(k) != 0); }
+  // ring offset of the partner voxel within a plane
+  __host__ __device__ static constexpr int off(int k) { return dy(k) * HX + dx(k); }
+  // ring cells of the box "tile - o_k" that are outside the tile
+  __host__ __device__ static constexpr int strip(int k) {
+    return TX * TY - (TY - (dy(k) != 0)) * (TX - (dx(k) != 0));
+  }
+};
+constexpr int sym_strip_total() {
+  int n = 0;
+  for (int k = 0; k < 13; ++k) n += HalfStencil::strip(k);
+  return n;
+}
+constexpr int NSTRIP = sym_strip_total();  // 340
+static_assert(NSTRIP > TX * TY && NSTRIP <= 2 * TX * TY, "one or two strip cliques per thread");
+constexpr int GSLOTS = 4 + 2 * 9;  // in-plane G, then two buffers of z+1 G
+
+// Strip clique i: packed (qa | qb << 10 | k << 20), qa/qb its ring cells; -1 if none.
+__device__ __forceinline__ int strip_item(int i) {
+  if (i >= NSTRIP) return -1;
+  int k = 0;
+#pragma unroll
+  for (int kk = 0; kk < 13; ++kk)
+    if (k == kk && i >= HalfStencil::strip(kk)) {
+      i -= HalfStencil::strip(kk);
+      ++k;
+    }
+  int dy = 0, dx = 0;
+#pragma unroll
+  for (int kk = 0; kk < 13; ++kk)
+    if (kk == k) {
+      dy = HalfStencil::dy(kk);
+      dx = HalfStencil::dx(kk);
+    }
+  int r, cc;
+  const int nrow = dy != 0 ? TX : 0;  // the ring row first (dy = +-1), then a ring column
+  if (i < nrow) {
+    r = dy == 1 ? -1 : TY;
+    cc = i - dx;
+  } else {
+    r = (dy == -1 ? 1 : 0) + (i - nrow);
+    cc = dx == 1 ? -1 : TX;
+  }
+  const int qa = (r + 1) * HX + cc + 1;
+  return qa | (qa + dy * HX + dx) << 10 | k << 20;
+}
+
+template <bool P2, bool NONNEG, bool EDGE>
+__device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP,
+                                               const float* __restrict__ Kf,
+                                               const float* __restrict__ Kfp,
+                                               const float* __restrict__ rstar,
+                                               float* __restrict__ f_new, double* partial, int nz,
+                                               int h, int w, float c, float lam, float inv_L,
+                                               int write_grad, const PriorConsts& pc, float* ysf,
+                                               float* gsf, double* red) {
+  using HS = HalfStencil;
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const int iy = blockIdx.x * TX + tx;
+  const int ix = blockIdx.y * TY + ty;
+  const long long nn = (long long)h * w;
+  const bool inside = ix < h && iy < w;
+  const int me = (ty + 1) * HX + tx + 1;  // own ring cell
+  HaloSlots hs;
+  hs.init(h, w);
+  // EDGE: neighbour bits (x-, x+, y-, y+, inside)
+  const int nbits = EDGE ? ((ix > 0) | (ix + 1 < h) << 1 | (iy > 0) << 2 | (iy + 1 < w) << 3 |
+                            inside << 4)
+                         : 0;
+  // weight of the clique between p and p + s*o_k (s = +1 forward, -1 backward)
+  auto wgt = [&](int k, int s) -> float {
+    const float wc = pc.w[HS::cls(k)];
+    if constexpr (!EDGE) {
+      return wc;
+    } else {
+      const int ddy = s * HS::dy(k), ddx = s * HS::dx(k);
+      const int need = 16 | (ddy < 0 ? 1 : ddy > 0 ? 2 : 0) | (ddx < 0 ? 4 : ddx > 0 ? 8 : 0);
+      return (nbits & need) == need ? wc : 0.f;
+    }
+  };
+  const int it0 = strip_item(threadIdx.x), it1 = strip_item(threadIdx.x + TX * TY);
+
+  float hf[2], hp[2];
+  auto fetch_plane = [&](int zz) {
+    const float* pf = F.at(zz, nz, nn);
+    const float* pp = FP.at(zz, nz, nn);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      hf[k] = hp[k] = 0.f;
+      if (hs.sm[k] >= 0 && pf && hs.off[k] >= 0) {
+        hf[k] = __ldg(pf + hs.off[k]);
+        hp[k] = __ldg(pp + hs.off[k]);
+      }
+    }
+  };
+  auto commit_plane = [&](int s) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (hs.sm[k] >= 0) ysf[s * HALO_ELEMS + hs.sm[k]] = fmaf(c, hf[k] - hp[k], hf[k]);
+  };
+  float nkf = 0.f, nkp = 0.f, nrs = 0.f;
+  auto fetch_ops = [&](int zz) {
+    if (!inside || zz >= nz) return;
+    const long long o = zz * nn + (long long)ix * w + iy;
+    if (Kf) {
+      nkf = __ldg(Kf + o);
+      nkp = __ldg(Kfp + o);
+    }
+    if (rstar) nrs = __ldg(rstar + o);
+  };
+  // one strip clique: y difference and where its G goes
+  auto strip_d = [&](int item, const float* y0, const float* y1) {
+    const int qa = item & 1023, qb = (item >> 10) & 1023;
+    return y0[qa] - ((item >> 20) >= 4 ? y1 : y0)[qb];
+  };
+  auto strip_dst = [&](int item, int s0) {
+    const int qa = item & 1023, k = item >> 20;
+    return k * HALO_ELEMS + qa + (k >= 4 ? 9 * HALO_ELEMS * s0 : 0);
+  };
+
+  const float glam = lam * pc.inv_sp;
+  const bool has_lo = FP.lo != nullptr;
+  double gsq = 0.0;
+  const int z0 = has_lo ? -1 : 0;
+  fetch_plane(z0);
+  commit_plane(z0 & 1);
+  fetch_plane(z0 + 1);
+  fetch_ops(0);
+  for (int z = z0; z < nz; ++z) {
+    const int s0 = z & 1, s1 = s0 ^ 1;
+    commit_plane(s1);
+    fetch_plane(z + 2);
+    const float kfv = nkf, kpv = nkp, rsv = nrs;
+    if (z >= 0) fetch_ops(z + 1);
+    __syncthreads();
+    // ---- phase A: own cliques (forward terms) and strip cliques -> shared memory
+    const float* y0 = ysf + s0 * HALO_ELEMS + me;
+    const float* y1 = ysf + s1 * HALO_ELEMS + me;
+    float* gin = gsf + me;                               // in-plane G of plane z
+    float* gcur = gsf + (4 + 9 * s0) * HALO_ELEMS + me;  // z+1 G of plane z
+    const float yv = y0[0];
+    const float2 yy = mk(yv, yv);
+    float f_in = 0.f, f_x = 0.f;
+#pragma unroll
+    for (int k = 0; k < 12; k += 2) {
+      const float a = (k < 4 ? y0 : y1)[HS::off(k)];
+      const float b = (k + 1 < 4 ? y0 : y1)[HS::off(k + 1)];
+      const float2 g = drho2<P2>(csub(yy, mk(a, b)), pc);
+      (k < 4 ? gin : gcur)[(k < 4 ? k : k - 4) * HALO_ELEMS] = g.x;
+      (k + 1 < 4 ? gin : gcur)[(k + 1 < 4 ? k + 1 : k - 3) * HALO_ELEMS] = g.y;
+      if (k < 4) {
+        f_in = fmaf(wgt(k, 1), g.x, f_in);
+        f_in = fmaf(wgt(k + 1, 1), g.y, f_in);
+      } else {
+        f_x = fmaf(wgt(k, 1), g.x, f_x);
+        f_x = fmaf(wgt(k + 1, 1), g.y, f_x);
+      }
+    }
+    {  // the 13th own clique with strip clique 0
+      const float* ya = ysf + s0 * HALO_ELEMS;
+      const float* yb = ysf + s1 * HALO_ELEMS;
+      const float2 g = drho2<P2>(mk(yv - y1[HS::off(12)], strip_d(it0, ya, yb)), pc);
+      gcur[8 * HALO_ELEMS] = g.x;
+      f_x = fmaf(wgt(12, 1), g.x, f_x);
+      gsf[strip_dst(it0, s0)] = g.y;
+      if (it1 >= 0) {
+        const float2 g1 = drho2<P2>(mk(strip_d(it1, ya, yb), 0.f), pc);
+        gsf[strip_dst(it1, s0)] = g1.x;
+      }
+    }
+    __syncthreads();
+    // ---- phase B: backward terms, gradient, update
+    if (z >= 0 && inside) {
+      float b_in = 0.f, b_x = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) b_in = fmaf(wgt(k, -1), gin[k * HALO_ELEMS - HS::off(k)], b_in);
+      if (z > 0 || has_lo) {
+        const float* gprev = gsf + (4 + 9 * s1) * HALO_ELEMS + me;  // z+1 G of plane z-1
+#pragma unroll
+        for (int k = 4; k < 13; ++k)
+          b_x = fmaf(wgt(k, -1), gprev[(k - 4) * HALO_ELEMS - HS::off(k)], b_x);
+      }
+      const bool hi_ok = z + 1 < nz || FP.hi != nullptr;
+      const float prior = (f_in - b_in) + ((hi_ok ? f_x : 0.f) - b_x);
+      const long long o = z * nn + (long long)ix * w + iy;
+      const float ky = fmaf(c, kfv - kpv, kfv);
+      const float grad = fmaf(glam, prior, ky - rsv);
+      if (write_grad) {
+        f_new[o] = grad;
+      } else {
+        float fn = fmaf(-grad, inv_L, yv);
+        if (NONNEG) fn = fmaxf(fn, 0.f);
+        f_new[o] = fn;
+      }
+      gsq = fma((double)grad, (double)grad, gsq);
+    }
+  }
+  const double r = block_sum_d<TX * TY>(gsq, red);
+  if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = r;
+}
+
+template <bool P2, bool NONNEG>
+__global__ void __launch_bounds__(TX* TY)
+k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const float* __restrict__ Kfp,
+                   const float* __restrict__ rstar, float* __restrict__ f_new,
+                   double* __restrict__ partial, int nz, int h, int w, float c, float lam,
+                   float inv_L, int write_grad, PriorConsts pc) {
+  __shared__ float ys[2 * HALO_ELEMS];
+  __shared__ float gs[GSLOTS * HALO_ELEMS];
+  __shared__ double red[TX * TY / 32];
+  const bool interior = blockIdx.y * TY >= 1 && (blockIdx.y + 1) * TY + 1 <= h &&
+                        blockIdx.x * TX >= 1 && (blockIdx.x + 1) * TX + 1 <= w;
+  if (interior)
+    prior_sym_tile<P2, NONNEG, false>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w, c, lam,
+                                      inv_L, write_grad, pc, ys, gs, red);
+  else
+    prior_sym_tile<P2, NONNEG, true>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w, c, lam,
+                                     inv_L, write_grad, pc, ys, gs, red);
+}
 // ============================================================ K5
 // partial[block*3 + {0,1,2}] = { E(f_new) (half stencil + halo_hi pairs),
 //   <f_new, K f_new / 2 - R*g>,  <f_new - f, (K f_new + K f)/2 - R*g> (0 if f null) }
@@ -466,7 +706,14 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
 #define TF_K4(TD, P2V, NN)                                                                    \
   k_prior_update<TD, P2V, NN><<<grid, TX * TY, 0, st>>>(F, FP, Kf, Kfp, rstar, f_new, partial, \
                                                          nz, h, w_, c, lam, inv_L, write_grad, pc)
-  if (three_d) {
+  static const int sym = getenv("TF_K4_SYM") ? atoi(getenv("TF_K4_SYM")) : 1;
+#define TF_K4S(P2V, NN)                                                                       \
+  k_prior_update_sym<P2V, NN><<<grid, TX * TY, 0, st>>>(F, FP, Kf, Kfp, rstar, f_new, partial, \
+                                                        nz, h, w_, c, lam, inv_L, write_grad, pc)
+  if (three_d && sym) {
+    if (p2) { if (nonneg) TF_K4S(true, true); else TF_K4S(true, false); }
+    else { if (nonneg) TF_K4S(false, true); else TF_K4S(false, false); }
+  } else if (three_d) {
     if (p2) { if (nonneg) TF_K4(true, true, true); else TF_K4(true, true, false); }
     else { if (nonneg) TF_K4(true, false, true); else TF_K4(true, false, false); }
   } else {
@@ -474,6 +721,7 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
     else { if (nonneg) TF_K4(false, false, true); else TF_K4(false, false, false); }
   }
 #undef TF_K4
+#undef TF_K4S
   TF_TRY(check_launch("k_prior_update"));
   k_sum_partials<<<1, 1024, 0, st>>>(partial, (int)(grid.x * grid.y), 1, out_gsq);
   return check_launch("k_sum_partials");
