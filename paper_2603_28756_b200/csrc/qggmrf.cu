@@ -19,6 +19,8 @@
 // (solver.py:149 and :157).  K5 returns, in fp64, E(f_new), the direct
 // fidelity <f_new, K f_new/2 - R*g> and the increment
 // <f_new - f, (K f_new + K f)/2 - R*g> used for the restart test.
+#include <type_traits>
+
 #include "tf_common.cuh"
 
 namespace tf {
@@ -308,70 +310,78 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
 //   grad_prior(p) = sum_k w_k(p, p+o_k) G_k(p) - sum_k w_k(p-o_k, p) G_k(p - o_k),
 //   G_k(q) = rho'(y_q - y_{q+o_k}),
 // over the 13 offsets o_k of the half stencil (4 in the plane, 9 towards z+1);
-// w is the clique weight times [both voxels in the slice].  Per plane step a
-// thread evaluates the 13 G of its own voxel (forward terms, summed in
-// registers) and 1-2 of the 340 "strip" G on the tile's one-voxel ring that
-// are backward terms of tile voxels; all go to shared memory unweighted, and
-// after a barrier each voxel adds its 13 weighted backward terms.  The z+1
-// cliques of plane z are the backward terms of plane z+1, so they are kept one
-// step (double buffer); with a slab halo below, a pre-step at z = -1 produces
-// the cliques between the halo plane and plane 0.  Half the log2/exp2 work of
-// k_prior_update, for ~30 more shared-memory accesses per voxel.  Tiles whose
-// ring lies inside the slice (all but the outermost) take weights straight from
-// the constant bank; edge tiles derive them from four neighbour bits.
-struct HalfStencil {
+// w is the clique weight times [both voxels in the slice].
+//
+// A CTA owns a 32 x (8 RY) column tile (RY voxels per thread, rows ty + 8 r).
+// Per plane step a thread evaluates the 13 G of each of its voxels (forward
+// terms, summed in registers) and 1-2 of the "strip" G on the tile's
+// one-voxel ring that are backward terms of tile voxels; all go to shared
+// memory unweighted, and after a barrier each voxel adds its 13 weighted
+// backward terms.  The z+1 cliques of plane z are the backward terms of plane
+// z+1, so they are kept one step (double buffer); with a slab halo below, a
+// pre-step at z = -1 produces the cliques between the halo plane and plane 0.
+// Half the log2/exp2 work of k_prior_update, for ~30 more shared-memory
+// accesses per voxel.  Tiles whose ring lies inside the slice (all but the
+// outermost) take weights straight from the constant bank; edge tiles derive
+// them from four neighbour bits.
+template <int RY>
+struct SymTile {
+  static constexpr int W = TX, H = TY * RY;       // tile
+  static constexpr int RW = W + 2, RH = H + 2;    // with the ring
+  static constexpr int CELLS = RW * RH;
+  static constexpr int NT = TX * TY;
+  static constexpr int SLOTS = (CELLS + NT - 1) / NT;  // ring cells staged per thread
   // (dy, dx): (0,1) (1,-1) (1,0) (1,1) in the plane, then (-1..1, -1..1) towards z+1
   __host__ __device__ static constexpr int dy(int k) { return k == 0 ? 0 : k < 4 ? 1 : (k - 4) / 3 - 1; }
   __host__ __device__ static constexpr int dx(int k) { return k == 0 ? 1 : k < 4 ? k - 2 : (k - 4) % 3 - 1; }
   // weight class: number of nonzero components of (dz, dy, dx)
   __host__ __device__ static constexpr int cls(int k) { return (k >= 4) + (dy(k) != 0) + (dx(k) != 0); }
-  // ring offset of the partner voxel within a plane
-  __host__ __device__ static constexpr int off(int k) { return dy(k) * HX + dx(k); }
+  // ring-cell offset of the partner voxel within a plane
+  __host__ __device__ static constexpr int off(int k) { return dy(k) * RW + dx(k); }
   // ring cells of the box "tile - o_k" that are outside the tile
   __host__ __device__ static constexpr int strip(int k) {
-    return TX * TY - (TY - (dy(k) != 0)) * (TX - (dx(k) != 0));
+    return W * H - (H - (dy(k) != 0)) * (W - (dx(k) != 0));
+  }
+  __host__ __device__ static constexpr int strips() {
+    int n = 0;
+    for (int k = 0; k < 13; ++k) n += strip(k);
+    return n;
+  }
+  static constexpr int GSLOTS = 4 + 2 * 9;  // in-plane G, then two buffers of z+1 G
+  static_assert(strips() <= 2 * NT, "at most two strip cliques per thread");
+
+  // strip clique i: packed (qa | qb << 11 | k << 22), qa / qb its ring cells; -1 if none
+  __device__ static int strip_item(int i) {
+    if (i >= strips()) return -1;
+    int k = 0;
+#pragma unroll
+    for (int kk = 0; kk < 13; ++kk)
+      if (k == kk && i >= strip(kk)) {
+        i -= strip(kk);
+        ++k;
+      }
+    int ddy = 0, ddx = 0;
+#pragma unroll
+    for (int kk = 0; kk < 13; ++kk)
+      if (kk == k) {
+        ddy = dy(kk);
+        ddx = dx(kk);
+      }
+    int r, cc;
+    const int nrow = ddy != 0 ? W : 0;  // the ring row first (dy = +-1), then a ring column
+    if (i < nrow) {
+      r = ddy == 1 ? -1 : H;
+      cc = i - ddx;
+    } else {
+      r = (ddy == -1 ? 1 : 0) + (i - nrow);
+      cc = ddx == 1 ? -1 : W;
+    }
+    const int qa = (r + 1) * RW + cc + 1;
+    return qa | (qa + ddy * RW + ddx) << 11 | k << 22;
   }
 };
-constexpr int sym_strip_total() {
-  int n = 0;
-  for (int k = 0; k < 13; ++k) n += HalfStencil::strip(k);
-  return n;
-}
-constexpr int NSTRIP = sym_strip_total();  // 340
-static_assert(NSTRIP > TX * TY && NSTRIP <= 2 * TX * TY, "one or two strip cliques per thread");
-constexpr int GSLOTS = 4 + 2 * 9;  // in-plane G, then two buffers of z+1 G
 
-// Strip clique i: packed (qa | qb << 10 | k << 20), qa/qb its ring cells; -1 if none.
-__device__ __forceinline__ int strip_item(int i) {
-  if (i >= NSTRIP) return -1;
-  int k = 0;
-#pragma unroll
-  for (int kk = 0; kk < 13; ++kk)
-    if (k == kk && i >= HalfStencil::strip(kk)) {
-      i -= HalfStencil::strip(kk);
-      ++k;
-    }
-  int dy = 0, dx = 0;
-#pragma unroll
-  for (int kk = 0; kk < 13; ++kk)
-    if (kk == k) {
-      dy = HalfStencil::dy(kk);
-      dx = HalfStencil::dx(kk);
-    }
-  int r, cc;
-  const int nrow = dy != 0 ? TX : 0;  // the ring row first (dy = +-1), then a ring column
-  if (i < nrow) {
-    r = dy == 1 ? -1 : TY;
-    cc = i - dx;
-  } else {
-    r = (dy == -1 ? 1 : 0) + (i - nrow);
-    cc = dx == 1 ? -1 : TX;
-  }
-  const int qa = (r + 1) * HX + cc + 1;
-  return qa | (qa + dy * HX + dx) << 10 | k << 20;
-}
-
-template <bool P2, bool NONNEG, bool EDGE>
+template <int RY, bool P2, bool NONNEG, bool EDGE>
 __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP,
                                                const float* __restrict__ Kf,
                                                const float* __restrict__ Kfp,
@@ -380,169 +390,253 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
                                                int h, int w, float c, float lam, float inv_L,
                                                int write_grad, const PriorConsts& pc, float* ysf,
                                                float* gsf, double* red) {
-  using HS = HalfStencil;
+  using S = SymTile<RY>;
+  constexpr int CELLS = S::CELLS, NT = S::NT;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const int iy = blockIdx.x * TX + tx;
-  const int ix = blockIdx.y * TY + ty;
+  const int gx0 = blockIdx.y * S::H, gy0 = blockIdx.x * S::W;
+  const int iy = gy0 + tx;
   const long long nn = (long long)h * w;
-  const bool inside = ix < h && iy < w;
-  const int me = (ty + 1) * HX + tx + 1;  // own ring cell
-  HaloSlots hs;
-  hs.init(h, w);
-  // EDGE: neighbour bits (x-, x+, y-, y+, inside)
-  const int nbits = EDGE ? ((ix > 0) | (ix + 1 < h) << 1 | (iy > 0) << 2 | (iy + 1 < w) << 3 |
-                            inside << 4)
-                         : 0;
-  // weight of the clique between p and p + s*o_k (s = +1 forward, -1 backward)
-  auto wgt = [&](int k, int s) -> float {
-    const float wc = pc.w[HS::cls(k)];
+  const int me0 = (ty + 1) * S::RW + tx + 1;  // own ring cell of row r: me0 + r TY RW
+  bool inside[RY];
+  int vo[RY];     // own in-plane offsets
+  int nbits[RY];  // EDGE: neighbour bits (x-, x+, y-, y+, inside)
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    const int ix = gx0 + ty + TY * r;
+    inside[r] = !EDGE || (ix < h && iy < w);
+    vo[r] = ix * w + iy;
+    nbits[r] = (ix > 0) | (ix + 1 < h) << 1 | (iy > 0) << 2 | (iy + 1 < w) << 3 | inside[r] << 4;
+  }
+  // ring cells this thread stages (cell threadIdx + m NT) and their in-plane offsets
+  int coff[S::SLOTS];
+#pragma unroll
+  for (int m = 0; m < S::SLOTS; ++m) {
+    const int e = threadIdx.x + m * NT;
+    const int ly = e / S::RW, lx = e - ly * S::RW;
+    const int gx = gx0 + ly - 1, gy = gy0 + lx - 1;
+    coff[m] = (e < CELLS && gx >= 0 && gx < h && gy >= 0 && gy < w) ? gx * w + gy : -1;
+  }
+  constexpr bool LAST_PARTIAL = CELLS % NT != 0;
+  const bool last_ok = !LAST_PARTIAL || threadIdx.x + (S::SLOTS - 1) * NT < CELLS;
+  // weight of the clique between voxel r and voxel r + s*o_k (s = +1 forward, -1 backward)
+  auto wgt = [&](int r, int k, int s) -> float {
+    const float wc = pc.w[S::cls(k)];
     if constexpr (!EDGE) {
       return wc;
     } else {
-      const int ddy = s * HS::dy(k), ddx = s * HS::dx(k);
+      const int ddy = s * S::dy(k), ddx = s * S::dx(k);
       const int need = 16 | (ddy < 0 ? 1 : ddy > 0 ? 2 : 0) | (ddx < 0 ? 4 : ddx > 0 ? 8 : 0);
-      return (nbits & need) == need ? wc : 0.f;
+      return (nbits[r] & need) == need ? wc : 0.f;
     }
   };
-  const int it0 = strip_item(threadIdx.x), it1 = strip_item(threadIdx.x + TX * TY);
+  const int it0 = S::strip_item(threadIdx.x), it1 = S::strip_item(threadIdx.x + NT);
 
-  float hf[2], hp[2];
+  float hf[S::SLOTS], hp[S::SLOTS];
   auto fetch_plane = [&](int zz) {
     const float* pf = F.at(zz, nz, nn);
     const float* pp = FP.at(zz, nz, nn);
+    const bool ok = pf != nullptr;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      hf[k] = hp[k] = 0.f;
-      if (hs.sm[k] >= 0 && pf && hs.off[k] >= 0) {
-        hf[k] = __ldg(pf + hs.off[k]);
-        hp[k] = __ldg(pp + hs.off[k]);
+    for (int m = 0; m < S::SLOTS; ++m) {
+      const bool v = ok && coff[m] >= 0;
+      hf[m] = v ? __ldg(pf + coff[m]) : 0.f;
+      hp[m] = v ? __ldg(pp + coff[m]) : 0.f;
+    }
+  };
+  auto fetch_ops = [&](int zz, float (&o)[3][RY]) {
+    if (zz >= nz) return;
+    const long long base = zz * nn;
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      if (Kf) {
+        o[0][r] = inside[r] ? __ldg(Kf + base + vo[r]) : 0.f;
+        o[1][r] = inside[r] ? __ldg(Kfp + base + vo[r]) : 0.f;
       }
+      if (rstar) o[2][r] = inside[r] ? __ldg(rstar + base + vo[r]) : 0.f;
     }
-  };
-  auto commit_plane = [&](int s) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (hs.sm[k] >= 0) ysf[s * HALO_ELEMS + hs.sm[k]] = fmaf(c, hf[k] - hp[k], hf[k]);
-  };
-  float nkf = 0.f, nkp = 0.f, nrs = 0.f;
-  auto fetch_ops = [&](int zz) {
-    if (!inside || zz >= nz) return;
-    const long long o = zz * nn + (long long)ix * w + iy;
-    if (Kf) {
-      nkf = __ldg(Kf + o);
-      nkp = __ldg(Kfp + o);
-    }
-    if (rstar) nrs = __ldg(rstar + o);
-  };
-  // one strip clique: y difference and where its G goes
-  auto strip_d = [&](int item, const float* y0, const float* y1) {
-    const int qa = item & 1023, qb = (item >> 10) & 1023;
-    return y0[qa] - ((item >> 20) >= 4 ? y1 : y0)[qb];
-  };
-  auto strip_dst = [&](int item, int s0) {
-    const int qa = item & 1023, k = item >> 20;
-    return k * HALO_ELEMS + qa + (k >= 4 ? 9 * HALO_ELEMS * s0 : 0);
   };
 
   const float glam = lam * pc.inv_sp;
   const bool has_lo = FP.lo != nullptr;
   double gsq = 0.0;
-  const int z0 = has_lo ? -1 : 0;
-  fetch_plane(z0);
-  commit_plane(z0 & 1);
-  fetch_plane(z0 + 1);
-  fetch_ops(0);
-  for (int z = z0; z < nz; ++z) {
-    const int s0 = z & 1, s1 = s0 ^ 1;
-    commit_plane(s1);
+  float opA[3][RY], opB[3][RY];
+#pragma unroll
+  for (int r = 0; r < RY; ++r) opA[0][r] = opA[1][r] = opA[2][r] = opB[0][r] = opB[1][r] = opB[2][r] = 0.f;
+
+  // One plane step; S0 = z & 1 is a compile-time constant, so every shared-memory
+  // offset below is an immediate.  `cur` holds this plane's operands, `nxt`
+  // receives the next plane's.
+  auto step = [&](auto s0c, int z, float (&cur)[3][RY], float (&nxt)[3][RY]) {
+    constexpr int S0 = decltype(s0c)::value, S1 = S0 ^ 1;
+    float* yw = ysf + S1 * CELLS + threadIdx.x;  // plane z+1 lands in slot S1
+#pragma unroll
+    for (int m = 0; m < S::SLOTS; ++m)
+      if (m + 1 < S::SLOTS || last_ok) yw[m * NT] = fmaf(c, hf[m] - hp[m], hf[m]);
     fetch_plane(z + 2);
-    const float kfv = nkf, kpv = nkp, rsv = nrs;
-    if (z >= 0) fetch_ops(z + 1);
+    fetch_ops(z + 1, nxt);
     __syncthreads();
     // ---- phase A: own cliques (forward terms) and strip cliques -> shared memory
-    const float* y0 = ysf + s0 * HALO_ELEMS + me;
-    const float* y1 = ysf + s1 * HALO_ELEMS + me;
-    float* gin = gsf + me;                               // in-plane G of plane z
-    float* gcur = gsf + (4 + 9 * s0) * HALO_ELEMS + me;  // z+1 G of plane z
-    const float yv = y0[0];
-    const float2 yy = mk(yv, yv);
-    float f_in = 0.f, f_x = 0.f;
+    const float* ya = ysf + S0 * CELLS;
+    const float* yb = ysf + S1 * CELLS;
+    float* gin = gsf;                          // in-plane G of plane z
+    float* gcur = gsf + (4 + 9 * S0) * CELLS;  // z+1 G of plane z
+    float yv[RY], f_in[RY], f_x[RY];
 #pragma unroll
-    for (int k = 0; k < 12; k += 2) {
-      const float a = (k < 4 ? y0 : y1)[HS::off(k)];
-      const float b = (k + 1 < 4 ? y0 : y1)[HS::off(k + 1)];
-      const float2 g = drho2<P2>(csub(yy, mk(a, b)), pc);
-      (k < 4 ? gin : gcur)[(k < 4 ? k : k - 4) * HALO_ELEMS] = g.x;
-      (k + 1 < 4 ? gin : gcur)[(k + 1 < 4 ? k + 1 : k - 3) * HALO_ELEMS] = g.y;
-      if (k < 4) {
-        f_in = fmaf(wgt(k, 1), g.x, f_in);
-        f_in = fmaf(wgt(k + 1, 1), g.y, f_in);
+    for (int r = 0; r < RY; ++r) {
+      yv[r] = ya[me0 + r * TY * S::RW];
+      f_in[r] = f_x[r] = 0.f;
+    }
+    auto strip_d = [&](int item) {
+      const int qa = item & 2047, qb = (item >> 11) & 2047;
+      return ya[qa] - ((item >> 22) >= 4 ? yb : ya)[qb];
+    };
+    auto strip_dst = [&](int item) {
+      const int qa = item & 2047, k = item >> 22;
+      return k * CELLS + qa + (k >= 4 ? 9 * CELLS * S0 : 0);
+    };
+    constexpr int NOWN = 13 * RY;
+    constexpr int NEVAL = (NOWN + 3) & ~1;  // + up to two strip cliques, even
+    float2 yy2 = mk(0.f, 0.f), nb2 = mk(0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < NEVAL; ++e) {
+      float yself, ynb;
+      if (e < NOWN) {
+        const int r = e / 13, k = e % 13;
+        yself = yv[r];
+        ynb = (k < 4 ? ya : yb)[me0 + r * TY * S::RW + S::off(k)];
       } else {
-        f_x = fmaf(wgt(k, 1), g.x, f_x);
-        f_x = fmaf(wgt(k + 1, 1), g.y, f_x);
+        const int item = e == NOWN ? it0 : e == NOWN + 1 ? it1 : -1;
+        if (item >= 0) {
+          const int qa = item & 2047, qb = (item >> 11) & 2047;
+          yself = ya[qa];
+          ynb = ((item >> 22) >= 4 ? yb : ya)[qb];
+        } else {
+          yself = ynb = 0.f;
+        }
+      }
+      if (e & 1) {
+        yy2.y = yself;
+        nb2.y = ynb;
+        const float2 g = drho2<P2>(csub(yy2, nb2), pc);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int ee = e - 1 + h2;
+          const float gv = h2 ? g.y : g.x;
+          if (ee < NOWN) {
+            const int r = ee / 13, k = ee % 13;
+            const int cell = me0 + r * TY * S::RW;
+            if (k < 4) {
+              gin[k * CELLS + cell] = gv;
+              f_in[r] = fmaf(wgt(r, k, 1), gv, f_in[r]);
+            } else {
+              gcur[(k - 4) * CELLS + cell] = gv;
+              f_x[r] = fmaf(wgt(r, k, 1), gv, f_x[r]);
+            }
+          } else {
+            const int item = ee == NOWN ? it0 : ee == NOWN + 1 ? it1 : -1;
+            if (item >= 0) gsf[strip_dst(item)] = gv;
+          }
+        }
+      } else {
+        yy2.x = yself;
+        nb2.x = ynb;
       }
     }
-    {  // the 13th own clique with strip clique 0
-      const float* ya = ysf + s0 * HALO_ELEMS;
-      const float* yb = ysf + s1 * HALO_ELEMS;
-      const float2 g = drho2<P2>(mk(yv - y1[HS::off(12)], strip_d(it0, ya, yb)), pc);
-      gcur[8 * HALO_ELEMS] = g.x;
-      f_x = fmaf(wgt(12, 1), g.x, f_x);
-      gsf[strip_dst(it0, s0)] = g.y;
-      if (it1 >= 0) {
-        const float2 g1 = drho2<P2>(mk(strip_d(it1, ya, yb), 0.f), pc);
-        gsf[strip_dst(it1, s0)] = g1.x;
-      }
-    }
+    (void)strip_d;
     __syncthreads();
     // ---- phase B: backward terms, gradient, update
-    if (z >= 0 && inside) {
-      float b_in = 0.f, b_x = 0.f;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) b_in = fmaf(wgt(k, -1), gin[k * HALO_ELEMS - HS::off(k)], b_in);
-      if (z > 0 || has_lo) {
-        const float* gprev = gsf + (4 + 9 * s1) * HALO_ELEMS + me;  // z+1 G of plane z-1
-#pragma unroll
-        for (int k = 4; k < 13; ++k)
-          b_x = fmaf(wgt(k, -1), gprev[(k - 4) * HALO_ELEMS - HS::off(k)], b_x);
-      }
+    if (z >= 0) {
+      const bool lo_ok = z > 0 || has_lo;
       const bool hi_ok = z + 1 < nz || FP.hi != nullptr;
-      const float prior = (f_in - b_in) + ((hi_ok ? f_x : 0.f) - b_x);
-      const long long o = z * nn + (long long)ix * w + iy;
-      const float ky = fmaf(c, kfv - kpv, kfv);
-      const float grad = fmaf(glam, prior, ky - rsv);
-      if (write_grad) {
-        f_new[o] = grad;
-      } else {
-        float fn = fmaf(-grad, inv_L, yv);
-        if (NONNEG) fn = fmaxf(fn, 0.f);
-        f_new[o] = fn;
+      const float* gprev = gsf + (4 + 9 * S1) * CELLS;  // z+1 G of plane z-1
+      float* outz = f_new + z * nn;
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const int cell = me0 + r * TY * S::RW;
+        float b_in = 0.f, b_x = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) b_in = fmaf(wgt(r, k, -1), gin[k * CELLS + cell - S::off(k)], b_in);
+        if (lo_ok) {
+#pragma unroll
+          for (int k = 4; k < 13; ++k)
+            b_x = fmaf(wgt(r, k, -1), gprev[(k - 4) * CELLS + cell - S::off(k)], b_x);
+        }
+        const float prior = (f_in[r] - b_in) + ((hi_ok ? f_x[r] : 0.f) - b_x);
+        const float ky = fmaf(c, cur[0][r] - cur[1][r], cur[0][r]);
+        const float grad = fmaf(glam, prior, ky - cur[2][r]);
+        if (inside[r]) {
+          if (write_grad) {
+            outz[vo[r]] = grad;
+          } else {
+            float fn = fmaf(-grad, inv_L, yv[r]);
+            if (NONNEG) fn = fmaxf(fn, 0.f);
+            outz[vo[r]] = fn;
+          }
+          gsq = fma((double)grad, (double)grad, gsq);
+        }
       }
-      gsq = fma((double)grad, (double)grad, gsq);
     }
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  // prologue: plane z0 into its slot, plane z0+1 in registers
+  const int z0 = has_lo ? -1 : 0;
+  fetch_plane(z0);
+  {
+    float* yw = ysf + (z0 & 1) * CELLS + threadIdx.x;
+#pragma unroll
+    for (int m = 0; m < S::SLOTS; ++m)
+      if (m + 1 < S::SLOTS || last_ok) yw[m * NT] = fmaf(c, hf[m] - hp[m], hf[m]);
   }
-  const double r = block_sum_d<TX * TY>(gsq, red);
+  fetch_plane(z0 + 1);
+  if (has_lo) step(I1{}, -1, opB, opA);  // cliques halo -> plane 0; fetches plane 0's operands
+  else fetch_ops(0, opA);
+  for (int z = 0; z < nz; z += 2) {
+    step(I0{}, z, opA, opB);
+    if (z + 1 < nz) step(I1{}, z + 1, opB, opA);
+  }
+  const double r = block_sum_d<NT>(gsq, red);
   if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = r;
 }
 
+#ifndef TF_K4_RY
+#define TF_K4_RY 2
+#endif
+#ifndef TF_K4_MINB
+#define TF_K4_MINB 3
+#endif
+constexpr int K4_RY = TF_K4_RY;
+
 template <bool P2, bool NONNEG>
-__global__ void __launch_bounds__(TX* TY)
+__global__ void __launch_bounds__(TX* TY, TF_K4_MINB)
 k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const float* __restrict__ Kfp,
                    const float* __restrict__ rstar, float* __restrict__ f_new,
                    double* __restrict__ partial, int nz, int h, int w, float c, float lam,
                    float inv_L, int write_grad, PriorConsts pc) {
-  __shared__ float ys[2 * HALO_ELEMS];
-  __shared__ float gs[GSLOTS * HALO_ELEMS];
+  using S = SymTile<K4_RY>;
+  extern __shared__ float sym_smem[];
   __shared__ double red[TX * TY / 32];
-  const bool interior = blockIdx.y * TY >= 1 && (blockIdx.y + 1) * TY + 1 <= h &&
-                        blockIdx.x * TX >= 1 && (blockIdx.x + 1) * TX + 1 <= w;
+  float* ys = sym_smem;                // [2][CELLS]
+  float* gs = sym_smem + 2 * S::CELLS;  // [GSLOTS][CELLS]
+  const bool interior = blockIdx.y * S::H >= 1 && (blockIdx.y + 1) * S::H + 1 <= h &&
+                        blockIdx.x * S::W >= 1 && (blockIdx.x + 1) * S::W + 1 <= w;
   if (interior)
-    prior_sym_tile<P2, NONNEG, false>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w, c, lam,
-                                      inv_L, write_grad, pc, ys, gs, red);
+    prior_sym_tile<K4_RY, P2, NONNEG, false>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w, c,
+                                             lam, inv_L, write_grad, pc, ys, gs, red);
   else
-    prior_sym_tile<P2, NONNEG, true>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w, c, lam,
-                                     inv_L, write_grad, pc, ys, gs, red);
+    prior_sym_tile<K4_RY, P2, NONNEG, true>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w, c,
+                                            lam, inv_L, write_grad, pc, ys, gs, red);
 }
+
+static size_t sym_smem_bytes() {
+  using S = SymTile<K4_RY>;
+  return sizeof(float) * (2 + S::GSLOTS) * S::CELLS;
+}
+static dim3 sym_grid(int h, int w) {
+  using S = SymTile<K4_RY>;
+  return dim3((w + S::W - 1) / S::W, (h + S::H - 1) / S::H);
+}
+
 // ============================================================ K5
 // partial[block*3 + {0,1,2}] = { E(f_new) (half stencil + halo_hi pairs),
 //   <f_new, K f_new / 2 - R*g>,  <f_new - f, (K f_new + K f)/2 - R*g> (0 if f null) }
@@ -707,9 +801,14 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
   k_prior_update<TD, P2V, NN><<<grid, TX * TY, 0, st>>>(F, FP, Kf, Kfp, rstar, f_new, partial, \
                                                          nz, h, w_, c, lam, inv_L, write_grad, pc)
   static const int sym = getenv("TF_K4_SYM") ? atoi(getenv("TF_K4_SYM")) : 1;
-#define TF_K4S(P2V, NN)                                                                       \
-  k_prior_update_sym<P2V, NN><<<grid, TX * TY, 0, st>>>(F, FP, Kf, Kfp, rstar, f_new, partial, \
-                                                        nz, h, w_, c, lam, inv_L, write_grad, pc)
+  const dim3 sgrid = sym_grid(h, w_);
+  const size_t ssmem = sym_smem_bytes();
+#define TF_K4S(P2V, NN)                                                                      \
+  do {                                                                                       \
+    TF_TRY(prep_kernel(k_prior_update_sym<P2V, NN>, ssmem));                                 \
+    k_prior_update_sym<P2V, NN><<<sgrid, TX * TY, ssmem, st>>>(                              \
+        F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, c, lam, inv_L, write_grad, pc);    \
+  } while (0)
   if (three_d && sym) {
     if (p2) { if (nonneg) TF_K4S(true, true); else TF_K4S(true, false); }
     else { if (nonneg) TF_K4S(false, true); else TF_K4S(false, false); }
@@ -723,7 +822,8 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
 #undef TF_K4
 #undef TF_K4S
   TF_TRY(check_launch("k_prior_update"));
-  k_sum_partials<<<1, 1024, 0, st>>>(partial, (int)(grid.x * grid.y), 1, out_gsq);
+  const int nparts = three_d && sym ? (int)(sgrid.x * sgrid.y) : (int)(grid.x * grid.y);
+  k_sum_partials<<<1, 1024, 0, st>>>(partial, nparts, 1, out_gsq);
   return check_launch("k_sum_partials");
 }
 

@@ -31,6 +31,17 @@ void timer_end(KernelTimer& t);
 
 inline bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
 
+// opt a kernel into more than 48 KB of dynamic shared memory
+template <typename K>
+inline int prep_kernel(K kern, size_t smem) {
+  if (smem > 48 * 1024) {
+    return check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem),
+                      "cudaFuncSetAttribute");
+  }
+  return TF_OK;
+}
+
 }  // namespace tf
 
 #define TF_TRY(expr)                 \

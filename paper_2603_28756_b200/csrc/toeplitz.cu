@@ -784,16 +784,6 @@ constexpr int cols_g() {  // columns per CTA in the generic K2
   return g < 1 ? 1 : g;
 }
 
-template <typename K>
-int prep_kernel(K kern, size_t smem) {
-  if (smem > 48 * 1024) {
-    TF_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem),
-                      "cudaFuncSetAttribute"));
-  }
-  return TF_OK;
-}
-
 template <int M, int NB>
 int launch_rows_fwd_t(const float* x, c32* T, int rows, int n_in, long long xs, long long xr,
                       long long nslices, cudaStream_t st) {
