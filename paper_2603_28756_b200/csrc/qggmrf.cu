@@ -763,6 +763,175 @@ k_sum_partials(const double* __restrict__ partial, int nblocks, int nv, double* 
   }
 }
 
+// ============================================================ K5, tiled (3-D, with the prior)
+// Same sums as k_energy_fid on the SymTile geometry of K4: a 32 x (8 RY) tile,
+// RY voxels per thread, the 13 half-stencil cliques of each voxel evaluated
+// two at a time (13 RY is even for RY = 2, so no lane idles), plane steps
+// unrolled by two so the ring slots are compile-time shared-memory offsets.
+template <int RY, bool P2, bool EDGE>
+__device__ __forceinline__ void energy_tile(const Planes& FN, const float* __restrict__ f,
+                                            const float* __restrict__ Kfn,
+                                            const float* __restrict__ Kf,
+                                            const float* __restrict__ rstar,
+                                            double* __restrict__ partial, int nz, int h, int w,
+                                            const PriorConsts& pc, float* xsf, double* red) {
+  using S = SymTile<RY>;
+  constexpr int CELLS = S::CELLS, NT = S::NT;
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const int gx0 = blockIdx.y * S::H, gy0 = blockIdx.x * S::W;
+  const int iy = gy0 + tx;
+  const long long nn = (long long)h * w;
+  const int me0 = (ty + 1) * S::RW + tx + 1;
+  bool inside[RY];
+  int vo[RY], nbits[RY];
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    const int ix = gx0 + ty + TY * r;
+    inside[r] = !EDGE || (ix < h && iy < w);
+    vo[r] = ix * w + iy;
+    nbits[r] = (ix > 0) | (ix + 1 < h) << 1 | (iy > 0) << 2 | (iy + 1 < w) << 3 | inside[r] << 4;
+  }
+  int coff[S::SLOTS];
+#pragma unroll
+  for (int m = 0; m < S::SLOTS; ++m) {
+    const int e = threadIdx.x + m * NT;
+    const int ly = e / S::RW, lx = e - ly * S::RW;
+    const int gx = gx0 + ly - 1, gy = gy0 + lx - 1;
+    coff[m] = (e < CELLS && gx >= 0 && gx < h && gy >= 0 && gy < w) ? gx * w + gy : -1;
+  }
+  const bool last_ok = CELLS % NT == 0 || threadIdx.x + (S::SLOTS - 1) * NT < CELLS;
+  auto wgt = [&](int r, int k) -> float {  // clique (p, p + o_k)
+    const float wc = pc.w[S::cls(k)];
+    if constexpr (!EDGE) {
+      return wc;
+    } else {
+      const int ddy = S::dy(k), ddx = S::dx(k);
+      const int need = 16 | (ddy < 0 ? 1 : ddy > 0 ? 2 : 0) | (ddx < 0 ? 4 : ddx > 0 ? 8 : 0);
+      return (nbits[r] & need) == need ? wc : 0.f;
+    }
+  };
+  float hv[S::SLOTS];
+  auto fetch_plane = [&](int zz) {
+    const float* pf = FN.at(zz, nz, nn);
+    const bool ok = pf != nullptr && zz <= nz;
+#pragma unroll
+    for (int m = 0; m < S::SLOTS; ++m) hv[m] = ok && coff[m] >= 0 ? __ldg(pf + coff[m]) : 0.f;
+  };
+  auto fetch_ops = [&](int zz, float (&o)[4][RY]) {
+    if (zz >= nz) return;
+    const long long base = zz * nn;
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      const bool in = inside[r];
+      o[0][r] = Kfn && in ? __ldg(Kfn + base + vo[r]) : 0.f;
+      o[1][r] = rstar && in ? __ldg(rstar + base + vo[r]) : 0.f;
+      o[2][r] = f && Kfn && in ? __ldg(f + base + vo[r]) : 0.f;
+      o[3][r] = f && Kfn && in ? __ldg(Kf + base + vo[r]) : 0.f;
+    }
+  };
+  auto commit = [&](int slot) {
+    float* xw = xsf + slot * CELLS + threadIdx.x;
+#pragma unroll
+    for (int m = 0; m < S::SLOTS; ++m)
+      if (m + 1 < S::SLOTS || last_ok) xw[m * NT] = hv[m];
+  };
+  double e_acc = 0.0, fid = 0.0, dfid = 0.0;
+  float opA[4][RY], opB[4][RY];
+#pragma unroll
+  for (int r = 0; r < RY; ++r)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) opA[j][r] = opB[j][r] = 0.f;
+
+  auto step = [&](auto s0c, int z, float (&cur)[4][RY], float (&nxt)[4][RY]) {
+    constexpr int S0 = decltype(s0c)::value, S1 = S0 ^ 1;
+    commit(S1);  // plane z+1 (zeros past an absent halo)
+    fetch_plane(z + 2);
+    fetch_ops(z + 1, nxt);
+    __syncthreads();
+    const float* xa = xsf + S0 * CELLS;
+    const float* xb = xsf + S1 * CELLS;
+    const float up = (z + 1 < nz || FN.hi != nullptr) ? 1.f : 0.f;
+    float xv[RY], acc[RY];
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      xv[r] = xa[me0 + r * TY * S::RW];
+      acc[r] = 0.f;
+    }
+    constexpr int NOWN = 13 * RY, NEVAL = (NOWN + 1) & ~1;
+    float2 x2 = mk(0.f, 0.f), n2 = mk(0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < NEVAL; ++e) {
+      float xs = 0.f, xn = 0.f;
+      if (e < NOWN) {
+        const int r = e / 13, k = e % 13;
+        xs = xv[r];
+        xn = (k < 4 ? xa : xb)[me0 + r * TY * S::RW + S::off(k)];
+      }
+      if (e & 1) {
+        x2.y = xs;
+        n2.y = xn;
+        const float2 g = rho2<P2>(csub(x2, n2), pc);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int ee = e - 1 + h2;
+          if (ee < NOWN) {
+            const int r = ee / 13, k = ee % 13;
+            acc[r] = fmaf(k < 4 ? wgt(r, k) : wgt(r, k) * up, h2 ? g.y : g.x, acc[r]);
+          }
+        }
+      } else {
+        x2.x = xs;
+        n2.x = xn;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      if (!inside[r]) continue;
+      const float fnv = xv[r], kfn = cur[0][r], rs = cur[1][r], fv = cur[2][r], kf = cur[3][r];
+      // fp32 products (one rounding, like the fp32 operands), fp64 running sums
+      if (Kfn) fid += (double)(fnv * fmaf(0.5f, kfn, -rs));
+      if (f && Kfn) dfid += (double)((fnv - fv) * (fmaf(0.5f, kfn + kf, 0.f) - rs));
+      e_acc += (double)(acc[r] * pc.inv_psp);
+    }
+    __syncthreads();  // slot S0 is overwritten by the next step's commit
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  fetch_plane(0);
+  commit(0);
+  fetch_plane(1);
+  fetch_ops(0, opA);
+  for (int z = 0; z < nz; z += 2) {
+    step(I0{}, z, opA, opB);
+    if (z + 1 < nz) step(I1{}, z + 1, opB, opA);
+  }
+  const int b = blockIdx.y * gridDim.x + blockIdx.x;
+  const double r0 = block_sum_d<NT>(e_acc, red);
+  const double r1 = block_sum_d<NT>(fid, red);
+  const double r2 = block_sum_d<NT>(dfid, red);
+  if (threadIdx.x == 0) {
+    partial[3 * b] = r0;
+    partial[3 * b + 1] = r1;
+    partial[3 * b + 2] = r2;
+  }
+}
+
+template <bool P2>
+__global__ void __launch_bounds__(TX* TY, TF_K4_MINB)
+k_energy_fid_t(Planes FN, const float* __restrict__ f, const float* __restrict__ Kfn,
+               const float* __restrict__ Kf, const float* __restrict__ rstar,
+               double* __restrict__ partial, int nz, int h, int w, PriorConsts pc) {
+  using S = SymTile<K4_RY>;
+  __shared__ float xs[2 * S::CELLS];
+  __shared__ double red[TX * TY / 32];
+  const bool interior = blockIdx.y * S::H >= 1 && (blockIdx.y + 1) * S::H + 1 <= h &&
+                        blockIdx.x * S::W >= 1 && (blockIdx.x + 1) * S::W + 1 <= w;
+  if (interior)
+    energy_tile<K4_RY, P2, false>(FN, f, Kfn, Kf, rstar, partial, nz, h, w, pc, xs, red);
+  else
+    energy_tile<K4_RY, P2, true>(FN, f, Kfn, Kf, rstar, partial, nz, h, w, pc, xs, red);
+}
+
 // ============================================================ host side
 static PriorConsts make_consts(double sigma, double p, double q, double T, const double* w3) {
   PriorConsts pc;
@@ -835,6 +1004,15 @@ int energy_fid(const float* fn, const float* fn_hi, const float* f, const float*
   const dim3 grid = tile_grid(h, w_);
   const Planes FN{fn, nullptr, fn_hi};
   const bool p2 = p == 2.0;
+  static const int tiled = getenv("TF_K5_TILED") ? atoi(getenv("TF_K5_TILED")) : 1;
+  if (three_d && with_prior && tiled) {
+    const dim3 sg = sym_grid(h, w_);
+    if (p2) k_energy_fid_t<true><<<sg, TX * TY, 0, st>>>(FN, f, Kfn, Kf, rstar, partial, nz, h, w_, pc);
+    else k_energy_fid_t<false><<<sg, TX * TY, 0, st>>>(FN, f, Kfn, Kf, rstar, partial, nz, h, w_, pc);
+    TF_TRY(check_launch("k_energy_fid_t"));
+    k_sum_partials<<<1, 1024, 0, st>>>(partial, (int)(sg.x * sg.y), 3, out3);
+    return check_launch("k_sum_partials");
+  }
   if (three_d) {
     if (p2) k_energy_fid<true, true><<<grid, TX * TY, 0, st>>>(FN, f, Kfn, Kf, rstar, partial, nz, h, w_, with_prior, pc);
     else k_energy_fid<true, false><<<grid, TX * TY, 0, st>>>(FN, f, Kfn, Kf, rstar, partial, nz, h, w_, with_prior, pc);
