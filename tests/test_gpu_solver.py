@@ -149,3 +149,45 @@ def test_divergence_raises(tf):
     with pytest.raises(FloatingPointError):
         tf.solve(ctx, prm, tf.SolverConfig(max_iters=400, tol=1e-300, lipschitz=1e-6, restart=False),
                  d["f0"][0])
+
+
+@pytest.mark.parametrize("shape", [(5, 72, 100), (3, 49, 161)])
+def test_prior_kernels_interior_tiles(tf, rng, shape):
+    """Slices larger than three K4/K5 tiles each way (interior + edge tiles, partial
+    last tiles) against the oracle, for the gradient with both halos, the fused
+    update and the energy / fidelity sums."""
+    import torch
+
+    import oracle as O
+
+    prm = tf.QggmrfParams(sigma=0.3, lam=0.7, p=2.0, q=1.2, T=1.0)
+    pr = O.Prior(sigma=0.3, lam=0.7)
+    s3 = tf.stencil_3d()
+    vol = rng.standard_normal(shape)
+    lo, hi = rng.standard_normal(shape[1:]), rng.standard_normal(shape[1:])
+    assert rel_l2(tf.prior_grad(prm, s3, vol, halo_lo=lo, halo_hi=hi),
+                  O.prior_grad(pr, vol, halo_lo=lo, halo_hi=hi)) < 1e-5
+    assert rel_l2(tf.prior_grad(prm, s3, vol), O.prior_grad(pr, vol)) < 1e-5
+    assert tf.prior_energy(prm, s3, vol, halo_hi=hi) == pytest.approx(
+        O.prior_energy(pr, vol, halo_hi=hi), rel=1e-5)
+    # fused update: f_new = y - (K y - R*g + lam grad_prior(y)) / L, y = f + c (f - fp)
+    from paper_2603_28756_b200.qggmrf import energy_fid, prior_update
+
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()  # noqa: E731
+    f, fp = vol, vol + 0.1 * rng.standard_normal(shape)
+    kf, kfp, rs = (rng.standard_normal(shape) for _ in range(3))
+    c, lam, inv_L = 0.4, 0.7, 0.05
+    out = torch.empty(shape, dtype=torch.float32, device="cuda")
+    gsq = prior_update(prm, s3, dev(f), dev(fp), out, kf=dev(kf), kfp=dev(kfp), rstar=dev(rs),
+                       c=c, lam=lam, inv_L=inv_L)
+    y = f + c * (f - fp)
+    grad = kf + c * (kf - kfp) - rs + lam * O.prior_grad(O.Prior(sigma=0.3, lam=1.0), y)
+    assert rel_l2(out.cpu().numpy(), y - inv_L * grad) < 1e-5
+    assert float(gsq) == pytest.approx(float(np.sum(grad ** 2)), rel=1e-4)
+    fn = out.cpu().numpy().astype(np.float64)
+    kfn = rng.standard_normal(shape)
+    e3 = energy_fid(prm, s3, dev(fn), f=dev(f), kfn=dev(kfn), kf=dev(kf), rstar=dev(rs)).cpu().numpy()
+    assert e3[0] == pytest.approx(O.prior_energy(O.Prior(sigma=0.3), fn), rel=1e-5)
+    assert e3[1] == pytest.approx(float(np.sum(fn * (0.5 * kfn - rs))), rel=1e-5, abs=1e-3)
+    assert e3[2] == pytest.approx(float(np.sum((fn - f) * (0.5 * (kfn + kf) - rs))), rel=1e-5,
+                                  abs=1e-3)
