@@ -86,6 +86,26 @@ int tf_prior_update(const float* d_f, const float* d_f_lo, const float* d_f_hi, 
                     double sigma, double p, double q, double T, const double* weights3,
                     double* d_ws, double* d_gsq, void* stream);
 
+/* tf_prior_update with the momentum coefficient read on the device: c = *d_c when
+ * d_c is not NULL (written by tf_solver_decide), so the host does not have to wait
+ * for the previous iteration's restart decision before launching the next. */
+int tf_prior_update_dc(const float* d_f, const float* d_f_lo, const float* d_f_hi,
+                       const float* d_fp, const float* d_fp_lo, const float* d_fp_hi,
+                       const float* d_Kf, const float* d_Kfp, const float* d_rstar, float* d_out,
+                       int nz, int h, int w, float c, const float* d_c, float lam, float inv_L,
+                       int nonneg, int write_grad, int three_d, double sigma, double p, double q,
+                       double T, const double* weights3, double* d_ws, double* d_gsq,
+                       void* stream);
+
+/* The restart / momentum / stop decision of one iteration, on the device
+ * (tomoforge/solver.py:147-180: restart when the objective increases, momentum
+ * t' = (1 + sqrt(1 + 4 t^2)) / 2, stop when |dobj| <= tol |obj| without a restart).
+ * d_vals = {E(f_new), sum grad^2, fidelity increment} (fp64);
+ * d_state = {obj, fid, prior, t, c} (fp64, updated in place); *d_c = next c (fp32);
+ * d_rec = {obj_new, fid_new, prior_new, sum grad^2, restarted, converged, finite, dobj}. */
+int tf_solver_decide(const double* d_vals, double* d_state, float* d_c, double* d_rec, double lam,
+                     int with_prior, int restart, double tol, void* stream);
+
 /* d_out3 (fp64) = { E(f_new) over the half stencil plus pairs into d_fn_hi
  *   (prior_energy, qggmrf.py:192-217; 0 if !with_prior),
  *   <f_new, K f_new / 2 - R*g>  (fidelity minus g'g/2, toeplitz.py:226-230),

@@ -108,7 +108,9 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
                  const float* rstar, float* f_new, int nz, int h, int w_, float c, float lam,
                  float inv_L, int nonneg, int write_grad, int three_d, double sigma, double p,
                  double q, double T, const double* w, double* partial, double* out_gsq,
-                 cudaStream_t st);
+                 const float* c_dev, cudaStream_t st);
+int solver_decide(const double* vals, double* state, float* c_out, double* rec, double lam,
+                  int with_prior, int restart, double tol, cudaStream_t st);
 int energy_fid(const float* fn, const float* fn_hi, const float* f, const float* Kfn,
                const float* Kf, const float* rstar, int nz, int h, int w_, int with_prior,
                int three_d, double sigma, double p, double q, double T, const double* w,
@@ -211,12 +213,32 @@ static int check_prior(int h, int w, int nz, double sigma, double p, double q, d
   return TF_OK;
 }
 
+int tf_prior_update_dc(const float* d_f, const float* d_f_lo, const float* d_f_hi,
+                       const float* d_fp, const float* d_fp_lo, const float* d_fp_hi,
+                       const float* d_Kf, const float* d_Kfp, const float* d_rstar, float* d_out,
+                       int nz, int h, int w, float c, const float* d_c, float lam, float inv_L,
+                       int nonneg, int write_grad, int three_d, double sigma, double p, double q,
+                       double T, const double* weights3, double* d_ws, double* d_gsq,
+                       void* stream);
+
 int tf_prior_update(const float* d_f, const float* d_f_lo, const float* d_f_hi, const float* d_fp,
                     const float* d_fp_lo, const float* d_fp_hi, const float* d_Kf,
                     const float* d_Kfp, const float* d_rstar, float* d_out, int nz, int h, int w,
                     float c, float lam, float inv_L, int nonneg, int write_grad, int three_d,
                     double sigma, double p, double q, double T, const double* weights3,
                     double* d_ws, double* d_gsq, void* stream) {
+  return tf_prior_update_dc(d_f, d_f_lo, d_f_hi, d_fp, d_fp_lo, d_fp_hi, d_Kf, d_Kfp, d_rstar,
+                            d_out, nz, h, w, c, nullptr, lam, inv_L, nonneg, write_grad, three_d,
+                            sigma, p, q, T, weights3, d_ws, d_gsq, stream);
+}
+
+int tf_prior_update_dc(const float* d_f, const float* d_f_lo, const float* d_f_hi,
+                       const float* d_fp, const float* d_fp_lo, const float* d_fp_hi,
+                       const float* d_Kf, const float* d_Kfp, const float* d_rstar, float* d_out,
+                       int nz, int h, int w, float c, const float* d_c, float lam, float inv_L,
+                       int nonneg, int write_grad, int three_d, double sigma, double p, double q,
+                       double T, const double* weights3, double* d_ws, double* d_gsq,
+                       void* stream) {
   TF_TRY(ensure_init());
   TF_TRY(check_prior(h, w, nz, sigma, p, q, T));
   if (!d_f || !d_fp || !d_out || !d_ws || !d_gsq || !weights3) return fail_arg("null pointer");
@@ -225,7 +247,16 @@ int tf_prior_update(const float* d_f, const float* d_f_lo, const float* d_f_hi, 
     return fail_arg("halo planes of f and f_prev must both be given");
   return prior_update(d_f, d_f_lo, d_f_hi, d_fp, d_fp_lo, d_fp_hi, d_Kf, d_Kfp, d_rstar, d_out, nz,
                       h, w, c, lam, inv_L, nonneg, write_grad, three_d, sigma, p, q, T, weights3, d_ws,
-                      d_gsq, (cudaStream_t)stream);
+                      d_gsq, d_c, (cudaStream_t)stream);
+}
+
+int tf_solver_decide(const double* d_vals, double* d_state, float* d_c, double* d_rec, double lam,
+                     int with_prior, int restart, double tol, void* stream) {
+  TF_TRY(ensure_init());
+  if (!d_vals || !d_state || !d_c || !d_rec) return fail_arg("null pointer");
+  if (!(tol > 0)) return fail_arg("tol must be positive");
+  return solver_decide(d_vals, d_state, d_c, d_rec, lam, with_prior, restart, tol,
+                       (cudaStream_t)stream);
 }
 
 int tf_energy_fid(const float* d_fn, const float* d_fn_hi, const float* d_f, const float* d_Kfn,

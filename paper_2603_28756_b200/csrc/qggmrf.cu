@@ -182,9 +182,10 @@ __global__ void __launch_bounds__(TX* TY)
 k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* __restrict__ Kfp,
                const float* __restrict__ rstar, float* __restrict__ f_new,
                double* __restrict__ partial, int nz, int h, int w, float c, float lam,
-               float inv_L, int write_grad, PriorConsts pc) {
+               float inv_L, int write_grad, PriorConsts pc, const float* __restrict__ c_dev) {
   __shared__ float ys[3][HY][HX];
   __shared__ double red[TX * TY / 32];
+  if (c_dev) c = *c_dev;  // momentum decided on the device (tf_solver_decide)
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int iy = blockIdx.x * TX + tx;  // contiguous axis
   const int ix = blockIdx.y * TY + ty;
@@ -631,9 +632,10 @@ __global__ void __launch_bounds__(TX* TY, TF_K4_MINB)
 k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const float* __restrict__ Kfp,
                    const float* __restrict__ rstar, float* __restrict__ f_new,
                    double* __restrict__ partial, int nz, int h, int w, float c, float lam,
-                   float inv_L, int write_grad, PriorConsts pc) {
+                   float inv_L, int write_grad, PriorConsts pc, const float* __restrict__ c_dev) {
   using S = SymTile<K4_RY>;
   extern __shared__ float sym_smem[];
+  if (c_dev) c = *c_dev;  // momentum decided on the device (tf_solver_decide)
   __shared__ double red[TX * TY / 32];
   float* ys = sym_smem;                // [2][CELLS]
   float* gs = sym_smem + 2 * S::CELLS;  // [GSLOTS][CELLS]
@@ -952,6 +954,46 @@ k_energy_fid_t(Planes FN, const float* __restrict__ f, const float* __restrict__
     energy_tile<K4_RY, P2, true>(FN, f, Kfn, Kf, rstar, partial, nz, h, w, pc, xs, red);
 }
 
+// ============================================================ solver decision (device)
+// One iteration's restart / momentum / stop decision (solver.py:147-180), the
+// same fp64 arithmetic as the host loop, so the iteration loop never waits on
+// the host.  vals = {E(f_new), sum grad^2, fidelity increment};
+// state = {obj, fid, prior, t, c}; rec = {obj_new, fid_new, prior_new,
+// sum grad^2, restarted, converged, finite, dobj}.
+__global__ void k_solver_decide(const double* __restrict__ vals, double* __restrict__ state,
+                                float* __restrict__ c_out, double* __restrict__ rec, double lam,
+                                int with_prior, int restart, double tol) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double e_new = with_prior ? vals[0] : 0.0, gsq = vals[1], dfid = vals[2];
+  const double obj = state[0], fid = state[1], prior = state[2], t = state[3];
+  const double dobj = dfid + lam * (e_new - prior);
+  const double obj_new = obj + dobj;
+  const bool restarted = restart && dobj > 0.0;
+  const double t_next = restarted ? 1.0 : (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+  const double c_next = restarted ? 0.0 : (t - 1.0) / t_next;
+  const bool converged = !restarted && fabs(dobj) <= tol * fabs(obj);
+  rec[0] = obj_new;
+  rec[1] = fid + dfid;
+  rec[2] = e_new;
+  rec[3] = gsq;
+  rec[4] = restarted ? 1.0 : 0.0;
+  rec[5] = converged ? 1.0 : 0.0;
+  rec[6] = isfinite(obj_new) ? 1.0 : 0.0;
+  rec[7] = dobj;
+  state[0] = obj_new;
+  state[1] = fid + dfid;
+  state[2] = e_new;
+  state[3] = t_next;
+  state[4] = c_next;
+  *c_out = (float)c_next;
+}
+
+int solver_decide(const double* vals, double* state, float* c_out, double* rec, double lam,
+                  int with_prior, int restart, double tol, cudaStream_t st) {
+  k_solver_decide<<<1, 32, 0, st>>>(vals, state, c_out, rec, lam, with_prior, restart, tol);
+  return check_launch("k_solver_decide");
+}
+
 // ============================================================ host side
 static PriorConsts make_consts(double sigma, double p, double q, double T, const double* w3) {
   PriorConsts pc;
@@ -981,14 +1023,15 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
                  const float* fp_lo, const float* fp_hi, const float* Kf, const float* Kfp,
                  const float* rstar, float* f_new, int nz, int h, int w_, float c, float lam, float inv_L,
                  int nonneg, int write_grad, int three_d, double sigma, double p, double q,
-                 double T, const double* w, double* partial, double* out_gsq, cudaStream_t st) {
+                 double T, const double* w, double* partial, double* out_gsq, const float* c_dev,
+                 cudaStream_t st) {
   const PriorConsts pc = make_consts(sigma, p, q, T, w);
   const dim3 grid = tile_grid(h, w_);
   const Planes F{f, f_lo, f_hi}, FP{fp, fp_lo, fp_hi};
   const bool p2 = p == 2.0;
 #define TF_K4(TD, P2V, NN)                                                                    \
   k_prior_update<TD, P2V, NN><<<grid, TX * TY, 0, st>>>(F, FP, Kf, Kfp, rstar, f_new, partial, \
-                                                         nz, h, w_, c, lam, inv_L, write_grad, pc)
+                                                         nz, h, w_, c, lam, inv_L, write_grad, pc, c_dev)
   static const int sym = getenv("TF_K4_SYM") ? atoi(getenv("TF_K4_SYM")) : 1;
   const dim3 sgrid = sym_grid(h, w_);
   const size_t ssmem = sym_smem_bytes();
@@ -996,7 +1039,7 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
   do {                                                                                       \
     TF_TRY(prep_kernel(k_prior_update_sym<P2V, NN>, ssmem));                                 \
     k_prior_update_sym<P2V, NN><<<sgrid, TX * TY, ssmem, st>>>(                              \
-        F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, c, lam, inv_L, write_grad, pc);    \
+        F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, c, lam, inv_L, write_grad, pc, c_dev); \
   } while (0)
   if (three_d && sym) {
     if (p2) { if (nonneg) TF_K4S(true, true); else TF_K4S(true, false); }

@@ -164,8 +164,9 @@ def _weights_ptr(stencil: NeighborStencil):
 
 def prior_update(params, stencil, f, fp, out, *, kf=None, kfp=None, rstar=None, c=0.0, lam=1.0,
                  inv_L=0.0, nonneg=False, write_grad=False, f_lo=None, f_hi=None, fp_lo=None,
-                 fp_hi=None) -> float:
-    """K4 launch on device stacks; returns sum(grad^2) (fp64)."""
+                 fp_hi=None, c_dev=None) -> torch.Tensor:
+    """K4 launch on device stacks; returns a device fp64 tensor [sum(grad^2)].
+    ``c_dev`` (fp32 device scalar) overrides ``c`` on the device (solver_decide)."""
     lib = _lib.ensure_ready()
     z, h, w_ = f.shape
     wsb = lib.tf_prior_workspace_bytes(h, w_)
@@ -173,12 +174,23 @@ def prior_update(params, stencil, f, fp, out, *, kf=None, kfp=None, rstar=None, 
     gsq = torch.empty(1, dtype=torch.float64, device=f.device)
     w, wp = _weights_ptr(stencil)
     P = _lib.ptr
-    _lib.check(lib.tf_prior_update(
+    _lib.check(lib.tf_prior_update_dc(
         P(f), P(f_lo), P(f_hi), P(fp), P(fp_lo), P(fp_hi), P(kf), P(kfp), P(rstar), P(out), z, h, w_,
-        float(c), float(lam), float(inv_L), int(bool(nonneg)), int(bool(write_grad)),
+        float(c), P(c_dev), float(lam), float(inv_L), int(bool(nonneg)), int(bool(write_grad)),
         int(stencil.three_d), *_consts(params), wp, ws.data_ptr(), gsq.data_ptr(),
-        _lib.stream_handle()), "tf_prior_update")
+        _lib.stream_handle()), "tf_prior_update_dc")
     return gsq
+
+
+def solver_decide(vals, state, c_dev, rec, *, lam, with_prior, restart, tol):
+    """Restart / momentum / stop decision of one iteration on the device
+    (tf_solver_decide): vals = [E_new, sum grad^2, dfid]; state = [obj, fid,
+    prior, t, c] updated in place; c_dev <- next c; rec <- the iteration's record."""
+    lib = _lib.ensure_ready()
+    P = _lib.ptr
+    _lib.check(lib.tf_solver_decide(P(vals), P(state), P(c_dev), P(rec), float(lam),
+                                    int(bool(with_prior)), int(bool(restart)), float(tol),
+                                    _lib.stream_handle()), "tf_solver_decide")
 
 
 def energy_fid(params, stencil, fn, *, fn_hi=None, f=None, kfn=None, kf=None, rstar=None,
