@@ -397,8 +397,22 @@ def _mbir(tf, args, world, rank):
     hier = tf.GridHierarchy(levels=(512, 1024, 2048), iters_per_level=(40, 20, 10))
     run_hier = lambda: tf.solve_hierarchical(  # noqa: E731
         sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300, lipschitz=L), use_fbp_init=True)
-    _, t_hier_cold = timed(run_hier)  # first call: per-level plans, PSFs, allocations
-    _, t_hier = timed(run_hier)
+    first, t_hier_cold = timed(run_hier)  # first call: per-level plans, PSFs, allocations
+    del first  # its page-locked result block goes back to the host cache for the next call
+    (hier_out, hier_recs), t_hier = timed(run_hier)
+    per_level = []
+    for lvl, recs in enumerate(hier_recs):
+        side = hier.levels[lvl]
+        factor = 1 << (len(hier.levels) - 1 - lvl)
+        slices = -(-hier_out.data.shape[0] // factor)  # ceil: the centred slice stride
+        # steady-state record intervals (the host runs one iteration ahead of the device)
+        steps = sorted(r.step_time for r in recs if r.iter >= 2)
+        ms = 1e3 * steps[len(steps) // 2] if steps else None
+        entry = {"side": side, "slices": slices, "iters": len(recs) - 1, "ms_per_iter_median": ms}
+        if ms and slices:
+            entry["hbm_frac_at_88B"] = bpv * slices * side * side / (ms / 1e3) / 1e9 / peak
+        per_level.append(entry)
+    del hier_out
     c1 = None if args.no_cpu_baseline else _c1_pipeline(tf, timed)
     return {
         "workload": f"C3 slab: {z} x 2048^2 per GPU, 128 angles, Nd=2048, qGGMRF lam=5e-4",
@@ -409,6 +423,7 @@ def _mbir(tf, args, world, rank):
         "solve_hbm_frac": bpv * vox / (per_it / 1e3) / 1e9 / peak,
         "hierarchical_3level_ms": t_hier,
         "hierarchical_3level_cold_ms": t_hier_cold,
+        "hierarchical_per_level": per_level,
         "hierarchical_schedule": "levels (512, 1024, 2048), iterations (40, 20, 10), FBP init, "
                                  "Lanczos-3 upsampling, L fixed from the finest level; "
                                  "second call (cold = first call of the process)",
