@@ -68,9 +68,12 @@ def as_stack(f, what: str = "input"):
 
 
 _CHUNK_ELEMS = 1 << 25  # 256 MB of float64 per staged copy
+# host float64 inputs are narrowed to fp32 by the staging threads (TF_STAGE_F32=0:
+# stage float64 and narrow on the device); bit-identical either way
+_STAGE_F32 = os.environ.get("TF_STAGE_F32", "1") != "0"
 
 
-_STAGE_THREADS = min(8, os.cpu_count() or 1)
+_STAGE_THREADS = int(os.environ.get("TF_STAGE_THREADS", min(8, os.cpu_count() or 1)))
 _stage_pool = None
 
 
@@ -101,7 +104,8 @@ def to_device(arr: np.ndarray) -> torch.Tensor:
         dst.copy_(torch.from_numpy(flat).to(dev))
         return out
     chunk = _CHUNK_ELEMS
-    tdt = torch.float64 if flat.dtype == np.float64 else torch.float32
+    # narrowed to fp32 by the host threads while staging (see pipelined_host_map)
+    tdt = torch.float64 if flat.dtype == np.float64 and not _STAGE_F32 else torch.float32
     stages = [torch.empty(chunk, dtype=tdt, pin_memory=True) for _ in range(2)]
     events = [None, None]
     stream = torch.cuda.current_stream()
@@ -109,7 +113,8 @@ def to_device(arr: np.ndarray) -> torch.Tensor:
     def fill(stage, lo, hi):
         part = (hi - lo) // _STAGE_THREADS + 1
         view = stage.numpy()
-        futs = [_pool().submit(np.copyto, view[a - lo:min(hi, a + part) - lo], flat[a:min(hi, a + part)])
+        futs = [_pool().submit(np.copyto, view[a - lo:min(hi, a + part) - lo], flat[a:min(hi, a + part)],
+                               "same_kind")
                 for a in range(lo, hi, part)]
         for f in futs:
             f.result()
@@ -127,23 +132,66 @@ def to_device(arr: np.ndarray) -> torch.Tensor:
     return out
 
 
+_PINNED_SIZES: set = set()  # result sizes already given a page-locked block
+_PIN_MIN_BYTES = 64 << 20
+_OUT_CHUNK = 1 << 23  # 64 MB of float64 per staged chunk
+
+
 def to_host64(t: torch.Tensor) -> np.ndarray:
     """fp32 device tensor -> float64 host array (widened on the device, chunked).
 
-    The result lives in page-locked memory from torch's caching host allocator
-    (the returned array keeps its tensor alive), so the device->host copy runs
-    at full link speed and repeated calls reuse the pinned block."""
+    Repeated results of one size live in page-locked memory from torch's caching
+    host allocator (the returned array keeps its tensor alive): the device->host
+    copy runs at link speed and later calls reuse the block.  The first result of
+    a large size goes to a pageable array through two small page-locked stages
+    (device copy of chunk i+1 overlapping the host threads' copy-out of chunk i),
+    because pinning a fresh multi-GB block costs far more than the copy."""
+    src = t.detach().reshape(-1)
+    nbytes = 8 * src.numel()
+    if nbytes >= _PIN_MIN_BYTES and nbytes not in _PINNED_SIZES:
+        _PINNED_SIZES.add(nbytes)
+        return _to_host64_staged(src).reshape(tuple(t.shape))
     try:
         out = torch.empty(tuple(t.shape), dtype=torch.float64, pin_memory=True)
     except RuntimeError:  # pinned memory exhausted: pageable fallback of the host buffer
-        out = torch.empty(tuple(t.shape), dtype=torch.float64)
+        return _to_host64_staged(src).reshape(tuple(t.shape))
     dst = out.reshape(-1)
-    src = t.detach().reshape(-1)
     for lo in range(0, src.numel(), _CHUNK_ELEMS):
         hi = min(src.numel(), lo + _CHUNK_ELEMS)
         dst[lo:hi].copy_(src[lo:hi].to(torch.float64), non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return out.numpy()
+
+
+def _to_host64_staged(src: torch.Tensor) -> np.ndarray:
+    out = np.empty(src.numel(), dtype=np.float64)
+    stages = [torch.empty(_OUT_CHUNK, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    pending = [None, None]  # (lo, hi, event) of the chunk in each stage
+
+    def drain(b):
+        lo, hi, ev = pending[b]
+        ev.synchronize()
+        view = stages[b].numpy()
+        part = (hi - lo) // _STAGE_THREADS + 1
+        futs = [_pool().submit(np.copyto, out[a:min(hi, a + part)], view[a - lo:min(hi, a + part) - lo])
+                for a in range(lo, hi, part)]
+        for f in futs:
+            f.result()
+        pending[b] = None
+
+    for i, lo in enumerate(range(0, src.numel(), _OUT_CHUNK)):
+        hi = min(src.numel(), lo + _OUT_CHUNK)
+        b = i % 2
+        if pending[b] is not None:
+            drain(b)
+        stages[b][:hi - lo].copy_(src[lo:hi].to(torch.float64), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        pending[b] = (lo, hi, ev)
+    for b in sorted(range(2), key=lambda b: pending[b][0] if pending[b] else 0):
+        if pending[b] is not None:
+            drain(b)
+    return out
 
 
 def wrap_like(kind: str, t: torch.Tensor):
@@ -184,7 +232,7 @@ def _wrap_host(kind: str, host: np.ndarray):
     return host
 
 
-_PIPE_SLICE_BYTES = 256 << 20
+_PIPE_SLICE_BYTES = int(os.environ.get("TF_PIPE_MB", 256)) << 20
 _streams: dict = {}
 
 
@@ -212,7 +260,10 @@ def pipelined_host_map(arr: np.ndarray, kind: str, fn):
         out = torch.empty(stack.shape, dtype=torch.float64, pin_memory=True)
     except RuntimeError:
         out = torch.empty(stack.shape, dtype=torch.float64)
-    stages = [torch.empty(step * plane, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    # the host threads narrow to fp32 while staging (round to nearest, as the device
+    # conversion would): half the upload bytes and half the staging writes
+    sdt = torch.float32 if _STAGE_F32 else torch.float64
+    stages = [torch.empty(step * plane, dtype=sdt, pin_memory=True) for _ in range(2)]
     staged = [None, None]
     caller = torch.cuda.current_stream()
     s_up, s_cmp, s_dn = _pipe_streams(dev)
@@ -227,13 +278,13 @@ def pipelined_host_map(arr: np.ndarray, kind: str, fn):
         view = stages[b].numpy()[: (z1 - z0) * plane]
         src = flat[z0:z1].reshape(-1)
         part = -(-src.size // _STAGE_THREADS)
-        futs = [_pool().submit(np.copyto, view[a:a + part], src[a:a + part])
+        futs = [_pool().submit(np.copyto, view[a:a + part], src[a:a + part], "same_kind")
                 for a in range(0, src.size, part)]
         for fu in futs:
             fu.result()
         with torch.cuda.stream(s_up):
-            x64 = stages[b][: view.size].to(dev, non_blocking=True)
-            x = x64.reshape((z1 - z0,) + stack.shape[1:]).to(torch.float32)
+            xs = stages[b][: view.size].to(dev, non_blocking=True)
+            x = xs.reshape((z1 - z0,) + stack.shape[1:]).to(torch.float32)
             ev = torch.cuda.Event()
             ev.record(s_up)
             staged[b] = ev

@@ -22,6 +22,7 @@ tables are built once per (plan, device) on the host in float64:
 
 from __future__ import annotations
 
+import collections
 import math
 from dataclasses import dataclass, field
 
@@ -172,6 +173,22 @@ class PlanTables:
         return ptr, ids.astype(np.int32)
 
 
+_TABLE_CACHE: "collections.OrderedDict[tuple, dict]" = collections.OrderedDict()
+_TABLE_CACHE_SIZE = 8
+
+
+def _shared_device_tables(key: tuple) -> dict:
+    """Per-geometry dict {device index: tables}, least-recently-used, 8 geometries."""
+    d = _TABLE_CACHE.get(key)
+    if d is None:
+        d = _TABLE_CACHE[key] = {}
+        while len(_TABLE_CACHE) > _TABLE_CACHE_SIZE:
+            _TABLE_CACHE.popitem(last=False)
+    else:
+        _TABLE_CACHE.move_to_end(key)
+    return d
+
+
 class NufftPlan:
     """Reusable type-1 plan for (grid side, polar sampling, tolerance) (nufft.py:104-168)."""
 
@@ -205,7 +222,11 @@ class NufftPlan:
         kx, ky = sampling.samples[:, 0], sampling.samples[:, 1]
         self._phase = np.exp(-1j * (kx + ky) * delta)
         self._tables = None
-        self._device_tables = {}
+        # device tables are shared by plans of the same geometry (repeated
+        # reconstructions, the per-level plans of solve_hierarchical)
+        self._device_tables = _shared_device_tables(
+            (self.grid_side, self.kernel_width, float(self.kernel_params), self.os_side,
+             sampling.radial_count, np.asarray(sampling.angles, dtype=np.float64).tobytes()))
 
     @property
     def sample_count(self) -> int:

@@ -12,6 +12,7 @@ M >= 2N-1 and runs the fused real-FFT convolution of csrc/toeplitz.cu
 
 from __future__ import annotations
 
+import collections
 import math
 import os
 from dataclasses import dataclass, field
@@ -100,13 +101,31 @@ def _check_tolerance(tolerance: float, oversampling: float) -> None:
         raise ValueError("oversampling factor must be >= 1.25")
 
 
+_PSF_CACHE: "collections.OrderedDict[tuple, PsfKernel]" = collections.OrderedDict()
+_PSF_CACHE_SIZE = 4  # ~100 MB of spectra each at N = 2048
+
+
 def _build(angles: np.ndarray, nd: int, source_side: int) -> PsfKernel:
-    lib = _lib.ensure_ready()
+    """The kernel of a geometry; immutable, so kernels of the same geometry (repeated
+    reconstructions, the levels of repeated hierarchical solves) are shared."""
     n = int(source_side)
     if n < 1:
         raise ValueError("source side must be positive")
-    m = fft_side_for(n)
     dev = _lib.device()
+    key = (dev.index, n, int(nd), np.asarray(angles, dtype=np.float64).tobytes())
+    psf = _PSF_CACHE.get(key)
+    if psf is None:
+        psf = _PSF_CACHE[key] = _build_new(angles, nd, n, dev)
+        while len(_PSF_CACHE) > _PSF_CACHE_SIZE:
+            _PSF_CACHE.popitem(last=False)
+    else:
+        _PSF_CACHE.move_to_end(key)
+    return psf
+
+
+def _build_new(angles: np.ndarray, nd: int, n: int, dev) -> PsfKernel:
+    lib = _lib.ensure_ready()
+    m = fft_side_for(n)
     cs = np.stack([np.cos(angles), np.sin(angles)], axis=1).astype(np.float64)
     d_cs = torch.from_numpy(np.ascontiguousarray(cs)).to(dev)
     h = m // 2 + 1
