@@ -191,3 +191,20 @@ def test_prior_kernels_interior_tiles(tf, rng, shape):
     assert e3[1] == pytest.approx(float(np.sum(fn * (0.5 * kfn - rs))), rel=1e-5, abs=1e-3)
     assert e3[2] == pytest.approx(float(np.sum((fn - f) * (0.5 * (kfn + kf) - rs))), rel=1e-5,
                                   abs=1e-3)
+
+
+@pytest.mark.parametrize("shape", [(1, 5, 7), (2, 1, 33), (3, 40, 1), (2, 17, 2), (1, 33, 48)])
+def test_prior_kernels_thin_slabs(tf, rng, shape):
+    """Degenerate tiles (one-voxel-wide slices, single-slice slabs with both halos as in
+    a distributed run with one slice per rank) against the oracle."""
+    import oracle as O
+
+    prm = tf.QggmrfParams(sigma=0.4, lam=1.0, p=1.8, q=1.1, T=1.3)
+    pr = O.Prior(sigma=0.4, lam=1.0, p=1.8, q=1.1, T=1.3)
+    s3 = tf.stencil_3d()
+    vol = rng.standard_normal(shape)
+    lo, hi = rng.standard_normal(shape[1:]), rng.standard_normal(shape[1:])
+    got = tf.prior_grad(prm, s3, vol, halo_lo=lo, halo_hi=hi)
+    assert rel_l2(got, O.prior_grad(pr, vol, halo_lo=lo, halo_hi=hi, three_d=True)) < 1e-5
+    assert tf.prior_energy(prm, s3, vol, halo_hi=hi) == pytest.approx(
+        O.prior_energy(pr, vol, halo_hi=hi, three_d=True), rel=1e-5)
