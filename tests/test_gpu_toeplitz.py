@@ -98,11 +98,13 @@ def test_apply_vs_oracle_midsize(tf, n, n_ang, nd):
     assert rel_l2(out, ref) < 1e-5
 
 
-def test_apply_2048_vs_oracle(tf):
-    """The bench size (C3/C4 slices): one 2048^2 slice, 128 angles, Nd=2048."""
+@pytest.mark.parametrize("nd", [2048, 2049])
+def test_apply_2048_vs_oracle(tf, nd):
+    """The bench size (C3/C4 slices): one 2048^2 slice, 128 angles, Nd = 2048 (even:
+    flip term active) and 2049 (odd), SURVEY.md §8d."""
     import oracle as O
 
-    n, nd = 2048, 2048
+    n = 2048
     ang = np.linspace(0, np.pi, 128, endpoint=False)
     x = np.random.default_rng(0).standard_normal((1, n, n))
     ref = O.apply_batch(O.build_psf(ang, nd, n), x)
