@@ -226,11 +226,31 @@ template <int M, int E, int G, bool AUXBULK, int NB>
 __global__ void __launch_bounds__(G*(M / E), (M >= 8192 ? 1 : 2))
 k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __restrict__ aux,
            int rows, int n_out, long long o_slice_stride, long long o_row_stride, float alpha,
-           float beta) {
+           float beta, int pf_dist) {
   constexpr int TT = M / E;
   constexpr int H = M / 2 + 1;
   constexpr int SB = group_stride(M, NB * G);
   constexpr int NR = 2 * NB;  // rows per group
+  // L2 prefetch for the CTA pf_dist blocks ahead (about one resident wave later):
+  // its spectrum block (and aux rows) are in L2 when it starts
+  if (pf_dist > 0 && threadIdx.x == 0) {
+    const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + pf_dist;
+    if (lin < (long long)gridDim.x * gridDim.y) {
+      const int zz = (int)(lin / gridDim.x), ux = (int)(lin - (long long)zz * gridDim.x);
+      const int nrb_ = nrb_of(rows);
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const int u = ux * G + gg;
+        const int rbr = NB == 2 ? u : u >> 1;
+        if (rbr >= nrb_ || (NB == 1 && (u & 1))) continue;
+        bulk_prefetch_l2(T + ((long long)zz * nrb_ + rbr) * H * RB, (uint32_t)(H * RB * sizeof(c32)));
+        if (AUXBULK)
+          for (int q = 0; q < RB && rbr * RB + q < rows; ++q)
+            bulk_prefetch_l2(aux + zz * o_slice_stride + (long long)(rbr * RB + q) * o_row_stride,
+                             (uint32_t)n_out * sizeof(float));
+      }
+    }
+  }
   static_assert(2 * H <= SB, "pair buffer must fit the exchange buffer");
   extern __shared__ __align__(16) c32 smem[];
   const int g = threadIdx.x / TT;
@@ -844,6 +864,14 @@ int launch_rows_fwd(const float* x, c32* T, int rows, int n_in, long long xs, lo
   return launch_rows_fwd_t<M, 2>(x, T, rows, n_in, xs, xr, nslices, st);
 }
 
+// How many blocks ahead a K3 CTA prefetches the spectrum block and aux rows into
+// L2 (TF_K3_L2PF, default one per SM: about half a resident wave ahead; 0 = off).
+// Measured on 64 x 2048^2: 0.92 -> 0.78 ms (110-200 equal, 592 thrashes).
+inline int k3_l2pf() {
+  static const int v = getenv("TF_K3_L2PF") ? atoi(getenv("TF_K3_L2PF")) : num_sms();
+  return v;
+}
+
 template <int M, int NB>
 int launch_rows_inv_t(const c32* T, float* out, const float* aux, int rows, int n_out,
                       long long os, long long orow, float alpha, float beta, long long nslices,
@@ -866,7 +894,7 @@ int launch_rows_inv_t(const c32* T, float* out, const float* aux, int rows, int 
     const int nz = (int)std::min<long long>(65535, nslices - z0);
     kern<<<dim3(gx, nz), G * TT, smem, st>>>(T + z0 * (long long)(M / 2 + 1) * RB * nrb_of(rows),
                                              out + z0 * os, aux ? aux + z0 * os : nullptr, rows,
-                                             n_out, os, orow, alpha, beta);
+                                             n_out, os, orow, alpha, beta, k3_l2pf());
   }
   timer_end(tm);
   return check_launch("k_rows_inv");
