@@ -143,24 +143,36 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
   const int t = threadIdx.x;
   const int nrb = nrb_of(rows);
   const uint32_t row_bytes = (uint32_t)n_in * sizeof(float);
-  auto issue = [&](long long u) {
-    const int z = (int)(u / nrb), rb = (int)(u - (long long)z * nrb);
-    const int r0 = rb * RB;
+  // (slice, row block) walks of the consumer and of the producer (one unit ahead),
+  // advanced by gridDim.x units without divisions
+  const int gz = (int)(gridDim.x / nrb), grb = (int)(gridDim.x - gz * nrb);
+  auto advance = [&](int& z, int& rb) {
+    z += gz;
+    rb += grb;
+    if (rb >= nrb) {
+      rb -= nrb;
+      ++z;
+    }
+  };
+  int pz = (int)(blockIdx.x / nrb), prb = (int)(blockIdx.x - (blockIdx.x / nrb) * nrb);
+  auto issue = [&]() {
+    const int r0 = prb * RB;
     const int nr = min(RB, rows - r0);
     mbar_expect_tx(full, nr * row_bytes);
     for (int q = 0; q < nr; ++q)
-      bulk_g2s(stage + q * n_in, x + z * x_slice_stride + (long long)(r0 + q) * x_row_stride,
+      bulk_g2s(stage + q * n_in, x + pz * x_slice_stride + (long long)(r0 + q) * x_row_stride,
                row_bytes, full);
+    advance(pz, prb);
   };
   if (t == 0) {
     mbar_init(full, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (t == 0 && (long long)blockIdx.x < nunits) issue(blockIdx.x);
+  if (t == 0 && (long long)blockIdx.x < nunits) issue();
   int it = 0;
-  for (long long u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
-    const int z = (int)(u / nrb), rb = (int)(u - (long long)z * nrb);
+  int z = (int)(blockIdx.x / nrb), rb = (int)(blockIdx.x - (blockIdx.x / nrb) * nrb);
+  for (long long u = blockIdx.x; u < nunits; u += gridDim.x, ++it, advance(z, rb)) {
     const int r0 = rb * RB;
     mbar_wait(full, (uint32_t)(it & 1));
     c32 v[NB][E];
@@ -180,7 +192,7 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
     __syncthreads();  // the stage is free: refill it with the next unit
     if (t == 0 && u + gridDim.x < nunits) {
       fence_proxy_async_smem();
-      issue(u + gridDim.x);
+      issue();
     }
     fftn<M, E, false, ZP, false, NB>(v, sm, SB, t);
 #pragma unroll
