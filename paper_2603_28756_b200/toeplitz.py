@@ -34,6 +34,7 @@ __all__ = [
     "toeplitz_apply",
     "fidelity_loss",
     "fidelity_grad",
+    "clear_caches",
 ]
 
 # slices processed per apply pass; bounds the half-spectrum workspace
@@ -103,6 +104,15 @@ def _check_tolerance(tolerance: float, oversampling: float) -> None:
 
 _PSF_CACHE: "collections.OrderedDict[tuple, PsfKernel]" = collections.OrderedDict()
 _PSF_CACHE_SIZE = 4  # ~100 MB of spectra each at N = 2048
+
+
+def clear_caches() -> None:
+    """Drop the per-geometry PSF kernels and NUFFT device tables (device memory:
+    ~100 MB of spectra per 2048^2 geometry)."""
+    from . import nufft
+
+    _PSF_CACHE.clear()
+    nufft._TABLE_CACHE.clear()
 
 
 def _build(angles: np.ndarray, nd: int, source_side: int) -> PsfKernel:

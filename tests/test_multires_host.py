@@ -65,3 +65,9 @@ def test_hierarchy_rules():
     d = default_hierarchy(256)
     assert d.levels == (64, 128, 256) and d.iters_per_level == (200, 100, 50)
     assert default_hierarchy(2048, 3, finest_iters=10).iters_per_level == (40, 20, 10)
+
+
+def test_clear_caches_is_exported():
+    import paper_2603_28756_b200 as tf
+
+    tf.clear_caches()  # no device work: only drops dictionary entries
