@@ -284,6 +284,7 @@ def run_ours(args, world, rank, local):
         "achieved": per_kernel[dom]["gbs"], "peak": peak["value"], "unit": "GB/s",
         "frac": per_kernel[dom]["frac"], "peak_source": peak["source"],
         "traffic": _ncu_traffic(dom),
+        "ncu_pipes": _ncu_json("ncu_pipes.json", dom),
         "per_kernel": per_kernel,
         "limiter_note": "k_cols_conv is FP32-FMA-pipe bound (ncu: FMA pipe ~67 %, top stall "
                         "math-pipe throttle; DRAM bytes equal the algorithmic bytes); see "
@@ -514,6 +515,14 @@ def _peak_hbm():
         return {"value": float(json.loads(p.read_text())["hbm_gbs"]), "source": "measured"}
     except Exception:  # noqa: BLE001
         return {"value": 6650.0, "source": "fallback"}
+
+
+def _ncu_json(name, kernel):
+    """Per-kernel entry of a committed ncu summary under profiles/ (None if absent)."""
+    try:
+        return json.loads((ROOT / "profiles" / name).read_text()).get(kernel)
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def _ncu_traffic(kernel):
