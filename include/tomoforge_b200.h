@@ -136,8 +136,10 @@ long long tf_nufft_workspace_bytes(int os, long long nslices);
 /* Type-1 NUFFT of nslices sample vectors (d_samples complex64, slice stride
  * sample_stride) onto the N x N grid, by Kaiser-Bessel gridding of width
  * `width` on an os x os grid (os a power of two, 32 <= os <= 8192, os >= 2N):
- *   d_tile_ptr / d_tile_idx : int32 CSR of the samples touching each 32 x 32
- *                             grid tile (tile = tb * (os/32) + ta), ascending
+ *   d_tile_ptr / d_tile_idx : int32 CSR of the samples whose window touches
+ *                             each 4-row band of each 32 x 32 grid tile (entry
+ *                             (tb * (os/32) + ta) * 8 + band; (os/32)^2 * 8 + 1
+ *                             pointers), samples ascending
  *   d_ab     : int32 [S][2] first window index (x, y), in [0, os)
  *   d_wts    : fp32 [S][2*width] Kaiser-Bessel weights (x taps, then y taps)
  *   d_prephase: complex64 [os] = e^{-2 pi i a (N/2) / os}

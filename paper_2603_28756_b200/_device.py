@@ -132,25 +132,19 @@ def to_device(arr: np.ndarray) -> torch.Tensor:
     return out
 
 
-_PINNED_SIZES: set = set()  # result sizes already given a page-locked block
-_PIN_MIN_BYTES = 64 << 20
 _OUT_CHUNK = 1 << 23  # 64 MB of float64 per staged chunk
 
 
 def to_host64(t: torch.Tensor) -> np.ndarray:
     """fp32 device tensor -> float64 host array (widened on the device, chunked).
 
-    Repeated results of one size live in page-locked memory from torch's caching
-    host allocator (the returned array keeps its tensor alive): the device->host
-    copy runs at link speed and later calls reuse the block.  The first result of
-    a large size goes to a pageable array through two small page-locked stages
-    (device copy of chunk i+1 overlapping the host threads' copy-out of chunk i),
-    because pinning a fresh multi-GB block costs far more than the copy."""
+    The result lives in page-locked memory from torch's caching host allocator
+    (the returned array keeps its tensor alive): the device->host copy runs at
+    link speed and, once the caller drops a result, the next call of that size
+    reuses the block (the first one pays for pinning it).  When page-locked
+    memory runs out the copy goes through two small staged chunks into a
+    pageable array."""
     src = t.detach().reshape(-1)
-    nbytes = 8 * src.numel()
-    if nbytes >= _PIN_MIN_BYTES and nbytes not in _PINNED_SIZES:
-        _PINNED_SIZES.add(nbytes)
-        return _to_host64_staged(src).reshape(tuple(t.shape))
     try:
         out = torch.empty(tuple(t.shape), dtype=torch.float64, pin_memory=True)
     except RuntimeError:  # pinned memory exhausted: pageable fallback of the host buffer

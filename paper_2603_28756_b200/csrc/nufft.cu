@@ -182,7 +182,8 @@ k_spread(const c32* __restrict__ c, long long c_stride, int nslices, int os, int
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[i][j] = mk(0.f, 0.f);
-  const int beg = __ldg(tile_ptr + tile), end = __ldg(tile_ptr + tile + 1);
+  // this warp's list: the samples whose window touches its 4-row band
+  const int beg = __ldg(tile_ptr + tile * 8 + warp), end = __ldg(tile_ptr + tile * 8 + warp + 1);
   // one-sample-ahead software pipeline: the index chain tile_idx -> ab -> weights /
   // values of sample q+1 is in flight while sample q accumulates
   int m_n = 0;

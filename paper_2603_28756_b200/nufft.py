@@ -48,6 +48,8 @@ _MAX_TOLERANCE = 1e-1
 _BETA_SCALE = {3: 0.94, 4: 0.96, 5: 0.97, 6: 0.98, 7: 0.985}
 _BETA_SCALE_DEFAULT = 0.99
 TILE = 32  # grid tile side of the spreading kernel (csrc/nufft.cu, k_spread)
+BAND = 4  # grid rows per warp of k_spread: the CSR lists samples per (tile, band)
+BANDS = TILE // BAND
 
 
 def kernel_width_for_tolerance(tolerance: float) -> int:
@@ -122,7 +124,7 @@ class PlanTables:
     deapodisation and the pre-phase are always built here."""
 
     def __init__(self, n: int, samples: np.ndarray, width: int, beta: float, os_side: int,
-                 weights: bool = True):
+                 weights: bool = True, csr: bool = True):
         g = gpu_grid_side(os_side)
         self.side, self.width, self.beta = n, width, beta
         self.grid = g
@@ -150,27 +152,60 @@ class PlanTables:
         self.deapod = (1.0 / dk).astype(np.float32)
         # output pixel ix sits at grid offset ix - N//2: shift it to ix (first N outputs)
         self.prephase = np.exp(-2j * np.pi * np.arange(g) * (n // 2) / g).astype(np.complex64)
-        self.tile_ptr, self.tile_idx = self._bin(a0, b0, g, width)
+        self.tile_ptr = self.tile_idx = None
+        if csr:
+            self.tile_ptr, self.tile_idx = self._bin(a0, b0, g, width)
 
     @staticmethod
     def _bin(a0, b0, g, width):
+        """CSR of the samples whose window touches each 4-row band of each 32 x 32
+        tile (entry tile * 8 + band, tile = tb * (g/32) + ta), samples ascending:
+        warp `band` of the tile's CTA walks only its own list."""
         nt = g // TILE
         m = np.arange(a0.size, dtype=np.int64)
         ta = [a0 // TILE, ((a0 + width - 1) % g) // TILE]
-        tb = [b0 // TILE, ((b0 + width - 1) % g) // TILE]
-        tiles, ids = [], []
+        rows = (b0[:, None] + np.arange(width)[None, :]) % g
+        bands = rows // BAND  # global band of each window row, (S, W)
+        first = np.ones_like(bands, dtype=bool)
+        first[:, 1:] = bands[:, 1:] != bands[:, :-1]  # each touched band once
+        keys, ids = [], []
         for i, xa in enumerate(ta):
             keep_a = np.ones(a0.size, bool) if i == 0 else xa != ta[0]
-            for j, xb in enumerate(tb):
-                keep = keep_a & (np.ones(a0.size, bool) if j == 0 else xb != tb[0])
-                tiles.append((xb * nt + xa)[keep])
-                ids.append(m[keep])
-        tiles = np.concatenate(tiles)
+            sel = first & keep_a[:, None]
+            gb = bands[sel]
+            tb, w = gb // BANDS, gb % BANDS
+            keys.append(((tb * nt + np.broadcast_to(xa[:, None], bands.shape)[sel]) * BANDS + w))
+            ids.append(np.broadcast_to(m[:, None], bands.shape)[sel])
+        keys = np.concatenate(keys)
         ids = np.concatenate(ids)
-        order = np.lexsort((ids, tiles))  # by tile, then sample index
-        tiles, ids = tiles[order], ids[order]
-        ptr = np.searchsorted(tiles, np.arange(nt * nt + 1)).astype(np.int32)
+        order = np.lexsort((ids, keys))  # by (tile, band), then sample index
+        keys, ids = keys[order], ids[order]
+        ptr = np.searchsorted(keys, np.arange(nt * nt * BANDS + 1)).astype(np.int32)
         return ptr, ids.astype(np.int32)
+
+
+def _band_csr_device(ab: torch.Tensor, g: int, width: int):
+    """PlanTables._bin on the device (torch stable sort; bit-identical CSR): the
+    samples whose window touches each (tile, 4-row band), in sample order."""
+    nt = g // TILE
+    a0, b0 = ab[:, 0].long(), ab[:, 1].long()
+    s = a0.numel()
+    ta0 = a0 // TILE
+    ta1 = ((a0 + width - 1) % g) // TILE
+    rows = (b0[:, None] + torch.arange(width, device=ab.device)) % g
+    bands = rows // BAND
+    first = torch.ones_like(bands, dtype=torch.bool)
+    first[:, 1:] = bands[:, 1:] != bands[:, :-1]
+    tb, w = bands // BANDS, bands % BANDS
+    k0 = torch.where(first, (tb * nt + ta0[:, None]) * BANDS + w, -1)
+    k1 = torch.where(first & (ta1 != ta0)[:, None], (tb * nt + ta1[:, None]) * BANDS + w, -1)
+    keys = torch.stack([k0, k1], dim=1).reshape(-1)  # sample-major: stable sort keeps order
+    ids = torch.arange(s, device=ab.device, dtype=torch.int32).repeat_interleave(2 * width)
+    ok = keys >= 0
+    keys, ids = keys[ok], ids[ok]
+    keys, order = torch.sort(keys, stable=True)
+    ptr = torch.searchsorted(keys, torch.arange(nt * nt * BANDS + 1, device=ab.device))
+    return ptr.to(torch.int32), ids[order].contiguous()
 
 
 _TABLE_CACHE: "collections.OrderedDict[tuple, dict]" = collections.OrderedDict()
@@ -257,7 +292,8 @@ class NufftPlan:
             lib = _lib.ensure_ready()
             samples = np.ascontiguousarray(self.sampling.samples, dtype=np.float64)
             h = self._tables or PlanTables(self.grid_side, samples, self.kernel_width,
-                                           self.kernel_params, self.os_side, weights=False)
+                                           self.kernel_params, self.os_side, weights=False,
+                                           csr=False)
             up = lambda a: torch.from_numpy(np.array(a, copy=True, order="C")).to(dev)  # noqa: E731
             kxy = up(samples)
             ab = torch.empty((samples.shape[0], 2), dtype=torch.int32, device=dev)
@@ -273,7 +309,8 @@ class NufftPlan:
             t = {
                 "ab": ab, "wts": wts, "deapod": up(h.deapod),
                 "prephase": up(h.prephase.view(np.float32)),
-                "tile_ptr": up(h.tile_ptr), "tile_idx": up(h.tile_idx),
+                **dict(zip(("tile_ptr", "tile_idx"), _band_csr_device(ab, self.gpu_side,
+                                                                       self.kernel_width))),
                 "sphase": None,
             }
             self._device_tables[dev.index] = t

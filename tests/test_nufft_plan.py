@@ -13,7 +13,7 @@ import pytest
 import oracle as O
 from conftest import golden, rel_l2
 from paper_2603_28756_b200.geometry import ScanGeometry, polar_sampling
-from paper_2603_28756_b200.nufft import TILE, NufftPlan
+from paper_2603_28756_b200.nufft import BAND, BANDS, TILE, NufftPlan
 
 
 def _plan(n, n_ang, nd, tol=1e-6, sigma=2.0):
@@ -59,20 +59,25 @@ def test_emulated_type1_matches_reference_fixture():
     assert rel_l2(got, d["type1"]) < 2e-6
 
 
-def test_tile_csr_covers_every_window():
+def test_band_csr_covers_every_window():
+    """k_spread's CSR: per (32 x 32 tile, 4-row band) the samples whose window
+    touches it, in sample order (deterministic per-point accumulation order)."""
     _, p = _plan(48, 12, 64)
     t = p.tables
     g, w, nt = t.grid, t.width, t.grid // TILE
     ptr, idx = t.tile_ptr, t.tile_idx
+    assert ptr.size == nt * nt * BANDS + 1
     assert ptr[0] == 0 and ptr[-1] == idx.size and np.all(np.diff(ptr) >= 0)
+    cols = (t.ab[:, 0:1] + np.arange(w)) % g
+    rows = (t.ab[:, 1:2] + np.arange(w)) % g
     for tile in range(nt * nt):
-        members = idx[ptr[tile]:ptr[tile + 1]]
-        assert np.all(np.diff(members) > 0)  # sample order kept -> deterministic sums
         ta, tb = tile % nt, tile // nt
-        a = (t.ab[:, 0:1] + np.arange(w)) % g // TILE
-        b = (t.ab[:, 1:2] + np.arange(w)) % g // TILE
-        touches = np.nonzero((a == ta).any(1) & (b == tb).any(1))[0]
-        np.testing.assert_array_equal(members, touches)
+        in_a = (cols // TILE == ta).any(1)
+        for band in range(BANDS):
+            members = idx[ptr[tile * BANDS + band]:ptr[tile * BANDS + band + 1]]
+            assert np.all(np.diff(members) > 0)
+            in_b = (rows // BAND == tb * BANDS + band).any(1)
+            np.testing.assert_array_equal(members, np.nonzero(in_a & in_b)[0])
 
 
 def _stockham(x, tw, L, r, nd):
@@ -142,3 +147,17 @@ def test_spread_kernel_table():
     beta, w = p.kernel_params, 7
     exact = np.i0(beta * np.sqrt(1 - (2 * x / w) ** 2))
     np.testing.assert_allclose(k(x), exact, rtol=1e-6)  # linear interpolation of the table
+
+
+@pytest.mark.parametrize("n,n_ang,nd", [(48, 12, 64), (33, 10, 33)])
+def test_band_csr_device_builder_matches_host(n, n_ang, nd):
+    """device_tables builds the CSR with torch (here on the CPU): identical to _bin."""
+    import torch
+
+    from paper_2603_28756_b200.nufft import _band_csr_device
+
+    _, p = _plan(n, n_ang, nd)
+    t = p.tables
+    ptr, idx = _band_csr_device(torch.from_numpy(t.ab), t.grid, t.width)
+    np.testing.assert_array_equal(ptr.numpy(), t.tile_ptr)
+    np.testing.assert_array_equal(idx.numpy(), t.tile_idx)
