@@ -515,7 +515,10 @@ template <int W>
 int launch_spread(const c32* c, long long c_stride, long long nz, int os, const int* tile_ptr,
                   const int* tile_idx, const int2* ab, const float* wts, const c32* preph,
                   c32* grid, cudaStream_t st) {
-  constexpr int NB = 4;
+#ifndef TF_SPREAD_NB
+#define TF_SPREAD_NB 2
+#endif
+  constexpr int NB = TF_SPREAD_NB;  // slices per CTA: amortises each sample's index chain
   const int nta = os / 32;
   const dim3 g((unsigned)(nta * nta), (unsigned)((nz + NB - 1) / NB));
   k_spread<W, NB><<<g, 256, 0, st>>>(c, c_stride, (int)nz, os, nta, tile_ptr, tile_idx, ab, wts,
