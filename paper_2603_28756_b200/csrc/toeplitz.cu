@@ -243,26 +243,6 @@ k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __re
   constexpr int H = M / 2 + 1;
   constexpr int SB = group_stride(M, NB * G);
   constexpr int NR = 2 * NB;  // rows per group
-  // L2 prefetch for the CTA pf_dist blocks ahead (about one resident wave later):
-  // its spectrum block (and aux rows) are in L2 when it starts
-  if (pf_dist > 0 && threadIdx.x == 0) {
-    const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + pf_dist;
-    if (lin < (long long)gridDim.x * gridDim.y) {
-      const int zz = (int)(lin / gridDim.x), ux = (int)(lin - (long long)zz * gridDim.x);
-      const int nrb_ = nrb_of(rows);
-#pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        const int u = ux * G + gg;
-        const int rbr = NB == 2 ? u : u >> 1;
-        if (rbr >= nrb_ || (NB == 1 && (u & 1))) continue;
-        bulk_prefetch_l2(T + ((long long)zz * nrb_ + rbr) * H * RB, (uint32_t)(H * RB * sizeof(c32)));
-        if (AUXBULK)
-          for (int q = 0; q < RB && rbr * RB + q < rows; ++q)
-            bulk_prefetch_l2(aux + zz * o_slice_stride + (long long)(rbr * RB + q) * o_row_stride,
-                             (uint32_t)n_out * sizeof(float));
-      }
-    }
-  }
   static_assert(2 * H <= SB, "pair buffer must fit the exchange buffer");
   extern __shared__ __align__(16) c32 smem[];
   const int g = threadIdx.x / TT;
@@ -300,6 +280,28 @@ k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __re
     }
   }
 
+  // L2 prefetch for the CTA pf_dist blocks ahead (about one resident wave later):
+  // its spectrum block (and aux rows) are in L2 when it starts
+  // issued after the CTA barrier by a warp other than the barrier initialiser, so
+  // no warp waits on it
+  if (pf_dist > 0 && threadIdx.x == (blockDim.x > 32 ? 32 : 0)) {
+    const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + pf_dist;
+    if (lin < (long long)gridDim.x * gridDim.y) {
+      const int zz = (int)(lin / gridDim.x), ux = (int)(lin - (long long)zz * gridDim.x);
+      const int nrb_ = nrb_of(rows);
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const int u = ux * G + gg;
+        const int rbr = NB == 2 ? u : u >> 1;
+        if (rbr >= nrb_ || (NB == 1 && (u & 1))) continue;
+        bulk_prefetch_l2(T + ((long long)zz * nrb_ + rbr) * H * RB, (uint32_t)(H * RB * sizeof(c32)));
+        if (AUXBULK)
+          for (int q = 0; q < RB && rbr * RB + q < rows; ++q)
+            bulk_prefetch_l2(aux + zz * o_slice_stride + (long long)(rbr * RB + q) * o_row_stride,
+                             (uint32_t)n_out * sizeof(float));
+      }
+    }
+  }
   auto fix = [&](int k, float4& y) {
     if (k == 0 || k == M / 2) { y.y = 0.f; y.w = 0.f; }  // irfft drops Im(DC, Nyquist)
   };
