@@ -268,7 +268,9 @@ k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __re
       mbar_init(abar, G);  // one arrival (with or without tx) per group
       fence_mbar_init();
     }
-    __syncthreads();
+    // with one group the initialising thread is the only one to arrive, and the
+    // other threads wait on the barrier only after the FFT's own CTA barriers
+    if constexpr (G > 1) __syncthreads();
     if (t == 0 && writer) {
       const int nr = min(NR, rows - r0);
       const uint32_t bytes = (uint32_t)n_out * sizeof(float);
