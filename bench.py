@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--slices", type=int, default=SLICES_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-mbir", action="store_true")
     return ap.parse_args()
 
