@@ -966,14 +966,16 @@ __global__ void k_solver_decide(const double* __restrict__ vals, double* __restr
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double e_new = with_prior ? vals[0] : 0.0, gsq = vals[1], dfid = vals[2];
   const double obj = state[0], fid = state[1], prior = state[2], t = state[3];
-  const double dobj = dfid + lam * (e_new - prior);
-  const double obj_new = obj + dobj;
+  // explicit roundings (no FMA contraction): the host's Python float arithmetic
+  const double dobj = __dadd_rn(dfid, __dmul_rn(lam, __dadd_rn(e_new, -prior)));
+  const double obj_new = __dadd_rn(obj, dobj);
   const bool restarted = restart && dobj > 0.0;
-  const double t_next = restarted ? 1.0 : (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+  const double t_next =
+      restarted ? 1.0 : __dadd_rn(1.0, sqrt(__dadd_rn(1.0, __dmul_rn(__dmul_rn(4.0, t), t)))) / 2.0;
   const double c_next = restarted ? 0.0 : (t - 1.0) / t_next;
   const bool converged = !restarted && fabs(dobj) <= tol * fabs(obj);
   rec[0] = obj_new;
-  rec[1] = fid + dfid;
+  rec[1] = __dadd_rn(fid, dfid);
   rec[2] = e_new;
   rec[3] = gsq;
   rec[4] = restarted ? 1.0 : 0.0;
@@ -981,7 +983,7 @@ __global__ void k_solver_decide(const double* __restrict__ vals, double* __restr
   rec[6] = isfinite(obj_new) ? 1.0 : 0.0;
   rec[7] = dobj;
   state[0] = obj_new;
-  state[1] = fid + dfid;
+  state[1] = __dadd_rn(fid, dfid);
   state[2] = e_new;
   state[3] = t_next;
   state[4] = c_next;

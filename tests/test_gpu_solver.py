@@ -208,3 +208,45 @@ def test_prior_kernels_thin_slabs(tf, rng, shape):
     assert rel_l2(got, O.prior_grad(pr, vol, halo_lo=lo, halo_hi=hi, three_d=True)) < 1e-5
     assert tf.prior_energy(prm, s3, vol, halo_hi=hi) == pytest.approx(
         O.prior_energy(pr, vol, halo_hi=hi, three_d=True), rel=1e-5)
+
+
+def test_device_decision_matches_host_arithmetic(tf, rng):
+    """tf_solver_decide reproduces the host loop's fp64 restart / momentum / stop
+    arithmetic (solver.py:158-180) bit for bit, over restarts, convergence and
+    non-finite objectives."""
+    import math
+
+    import torch
+
+    from paper_2603_28756_b200.qggmrf import solver_decide
+
+    lam, tol = 0.37, 1e-6
+    state = torch.tensor([10.0, 9.0, 2.7, 1.0, 0.0], dtype=torch.float64, device="cuda")
+    c_dev = torch.zeros(1, dtype=torch.float32, device="cuda")
+    obj, fid, prior, t = 10.0, 9.0, 2.7, 1.0
+    cases = [(rng.standard_normal(), abs(rng.standard_normal()), rng.standard_normal() * 1e-3)
+             for _ in range(40)]
+    cases += [(prior, 1.0, 0.0), (float("inf"), 1.0, -1.0)]  # dobj = 0 -> converged; inf
+    for restart in (True, False):
+        for e_new, gsq, dfid in cases:
+            vals = torch.tensor([e_new, gsq, dfid], dtype=torch.float64, device="cuda")
+            rec = torch.empty(8, dtype=torch.float64, device="cuda")
+            solver_decide(vals, state, c_dev, rec, lam=lam, with_prior=True, restart=restart,
+                          tol=tol)
+            r = rec.cpu().tolist()
+            dobj = dfid + lam * (e_new - prior)
+            obj_new = obj + dobj
+            rst = restart and dobj > 0.0
+            t_next = 1.0 if rst else (1.0 + math.sqrt(1.0 + 4.0 * t * t)) / 2.0
+            c_next = 0.0 if rst else (t - 1.0) / t_next
+            conv = (not rst) and abs(dobj) <= tol * abs(obj)
+            fin = math.isfinite(obj_new)
+            assert r[0] == obj_new or (not fin and not math.isfinite(r[0]))
+            assert r[1] == fid + dfid and r[3] == gsq and r[7] == dobj or not fin
+            assert bool(r[4]) == rst and bool(r[5]) == conv and bool(r[6]) == fin
+            assert float(c_dev.item()) == float(np.float32(c_next)) or not fin
+            if not fin:  # the solver raises here; restart the synthetic sequence
+                state.copy_(torch.tensor([10.0, 9.0, 2.7, 1.0, 0.0], dtype=torch.float64))
+                obj, fid, prior, t = 10.0, 9.0, 2.7, 1.0
+                continue
+            obj, fid, prior, t = obj_new, fid + dfid, e_new, t_next
