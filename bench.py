@@ -271,7 +271,7 @@ def run_ours(args, world, rank, local):
     names = {v: k for k, v in _lib.TIMER_SLOTS.items()}
     per_kernel = {names[s]: {"avg_ms": t / n, "launches": n} for s, (t, n) in kt.items() if s in names}
     launches = sum(v["launches"] for v in per_kernel.values())
-    ab = algorithmic_bytes(z, N_SIDE, psf.padded_side)
+    ab = algorithmic_bytes(z, N_SIDE, psf.fft_side)
     peak = _peak_hbm()
     for k, v in per_kernel.items():
         v["gbs"] = ab[k] / (v["avg_ms"] / 1e3) / 1e9

@@ -50,6 +50,13 @@ long long tf_psf_workspace_bytes(int M);
 int tf_psf_build(int n, int M, int n_angles, const double* d_cossin, int nd, void* d_PQ,
                  float* d_Bi, void* d_ws, long long ws_bytes, void* stream);
 
+/* The reference's lag kernel on its odd padded grid of side m (padded_side_for,
+ * toeplitz.py:53-60): d_out [m][m] fp64 = K(d) = sum_theta sum_j cos(w_j d.e_theta)
+ * (the adjoint NUFFT of unit weights, toeplitz.py:102), ifftshifted (lag d at
+ * d mod m).  fft2(d_out) is PsfKernel.spectrum (toeplitz.py:63-82). */
+int tf_psf_kernel(int m, int n_angles, const double* d_cossin, int nd, double* d_out,
+                  void* stream);
+
 /* out = alpha * (K x) + beta * aux over a stack of nslices N x N slices.
  * Replaces _apply_batch (toeplitz.py:134-149); with alpha=1, beta=-1, aux=R*g
  * it is fidelity_grad (toeplitz.py:233-241).  aux may be NULL.  x != out. */
@@ -78,6 +85,8 @@ long long tf_prior_workspace_bytes(int h, int w);
  * grad = K y - R*g + lam * sum_s b_s rho'(y_v - y_{v+s})  (prior_grad, qggmrf.py:172-189);
  * write_grad = 0: out = y - grad * inv_L (clamped at 0 if nonneg) -- solver.py:149-156;
  * write_grad = 1: out = grad.  d_Kf/d_Kfp/d_rstar may be NULL (treated as 0).
+ * d_out may alias d_Kfp (each voxel's K f_prev is read before its output is
+ * written; the solver keeps 4 volumes + R*g this way); no other aliasing.
  * *d_gsq = sum grad^2 (fp64). */
 int tf_prior_update(const float* d_f, const float* d_f_lo, const float* d_f_hi, const float* d_fp,
                     const float* d_fp_lo, const float* d_fp_hi, const float* d_Kf,

@@ -34,6 +34,7 @@ _SIGNATURES = {
     "tf_psf_workspace_bytes": (_c_ll, [_c_int]),
     "tf_psf_build": (_c_int, [_c_int, _c_int, _c_int, _c_void_p, _c_int, _c_void_p, _c_void_p,
                               _c_void_p, _c_ll, _c_void_p]),
+    "tf_psf_kernel": (_c_int, [_c_int, _c_int, _c_void_p, _c_int, _c_void_p, _c_void_p]),
     "tf_toeplitz_apply": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_float, _c_float, _c_ll,
                                    _c_int, _c_int, _c_void_p, _c_void_p, _c_int, _c_void_p,
                                    _c_ll, _c_void_p]),

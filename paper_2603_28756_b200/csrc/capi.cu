@@ -101,6 +101,7 @@ int toeplitz_apply(const float* x, float* out, const float* aux, float alpha, fl
 size_t psf_workspace_bytes(int M);
 int psf_build(int n, int M, const double* cs, int n_angles, int nd, void* PQ, float* Bi,
               void* ws, size_t ws_bytes, cudaStream_t st);
+int psf_kernel_grid(int m, const double* cs, int n_angles, int nd, double* out, cudaStream_t st);
 int reduce_blocks();
 long long prior_partials(int h, int w);
 int prior_update(const float* f, const float* f_lo, const float* f_hi, const float* fp,
@@ -172,6 +173,15 @@ int tf_psf_build(int n, int M, int n_angles, const double* d_cossin, int nd, voi
   if (!d_cossin || !d_PQ || !d_Bi || !d_ws) return fail_arg("null pointer");
   return psf_build(n, M, d_cossin, n_angles, nd, d_PQ, d_Bi, d_ws, (size_t)ws_bytes,
                    (cudaStream_t)stream);
+}
+
+int tf_psf_kernel(int m, int n_angles, const double* d_cossin, int nd, double* d_out,
+                  void* stream) {
+  TF_TRY(ensure_init());
+  if (m < 1 || m % 2 == 0 || m > 32768) return fail_arg("kernel grid side must be odd, got %d", m);
+  if (n_angles < 1 || nd < 1) return fail_arg("bad sampling (angles=%d, nd=%d)", n_angles, nd);
+  if (!d_cossin || !d_out) return fail_arg("null pointer");
+  return psf_kernel_grid(m, d_cossin, n_angles, nd, d_out, (cudaStream_t)stream);
 }
 
 int tf_toeplitz_apply(const float* d_x, float* d_out, const float* d_aux, float alpha,

@@ -179,8 +179,8 @@ struct InPlaneW {
 // the paired-fp32 datapath; per pair the XU runs only log2 and exp2.
 template <bool THREE_D, bool P2, bool NONNEG>
 __global__ void __launch_bounds__(TX* TY)
-k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* __restrict__ Kfp,
-               const float* __restrict__ rstar, float* __restrict__ f_new,
+k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* Kfp,
+               const float* __restrict__ rstar, float* f_new,
                double* __restrict__ partial, int nz, int h, int w, float c, float lam,
                float inv_L, int write_grad, PriorConsts pc, const float* __restrict__ c_dev) {
   __shared__ float ys[3][HY][HX];
@@ -226,7 +226,7 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* _
     const long long o = zz * nn + (long long)ix * w + iy;
     if (Kf) {
       nkf = __ldg(Kf + o);
-      nkp = __ldg(Kfp + o);
+      nkp = Kfp[o];  // plain load: Kfp may alias f_new (solver ring)
     }
     if (rstar) nrs = __ldg(rstar + o);
   };
@@ -403,9 +403,9 @@ struct SymTile {
 template <int RY, bool P2, bool NONNEG, bool EDGE>
 __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP,
                                                const float* __restrict__ Kf,
-                                               const float* __restrict__ Kfp,
+                                               const float* Kfp,  // may alias f_new
                                                const float* __restrict__ rstar,
-                                               float* __restrict__ f_new, double* partial, int nz,
+                                               float* f_new, double* partial, int nz,
                                                int h, int w, float c, float lam, float inv_L,
                                                int write_grad, const PriorConsts& pc, float* ysf,
                                                float* gsf, double* red) {
@@ -469,7 +469,7 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
     for (int r = 0; r < RY; ++r) {
       if (Kf) {
         o[0][r] = inside[r] ? __ldg(Kf + base + vo[r]) : 0.f;
-        o[1][r] = inside[r] ? __ldg(Kfp + base + vo[r]) : 0.f;
+        o[1][r] = inside[r] ? Kfp[base + vo[r]] : 0.f;  // may alias f_new
       }
       if (rstar) o[2][r] = inside[r] ? __ldg(rstar + base + vo[r]) : 0.f;
     }
@@ -629,8 +629,8 @@ constexpr int K4_RY = TF_K4_RY;
 
 template <bool P2, bool NONNEG>
 __global__ void __launch_bounds__(TX* TY, TF_K4_MINB)
-k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const float* __restrict__ Kfp,
-                   const float* __restrict__ rstar, float* __restrict__ f_new,
+k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const float* Kfp,
+                   const float* __restrict__ rstar, float* f_new,
                    double* __restrict__ partial, int nz, int h, int w, float c, float lam,
                    float inv_L, int write_grad, PriorConsts pc, const float* __restrict__ c_dev) {
   using S = SymTile<K4_RY>;

@@ -771,6 +771,31 @@ __global__ void k_psf_lags(float* __restrict__ kmain, float* __restrict__ kflip,
   kflip[id] = kf;
 }
 
+// The reference's lag kernel K(d) = Re type1(1 at every polar sample) on its odd
+// grid of side m (toeplitz.py:102-103, fp64 closed form), stored ifftshifted:
+// out[i0][i1] = K(d0, d1) with d = i for i <= (m-1)/2, else i - m.  Its fft2 is
+// the reference's PsfKernel.spectrum.
+__global__ void k_psf_kernel_grid(double* __restrict__ out, int m, const double* __restrict__ cs,
+                                  int n_angles, int nd) {
+  const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (id >= (long long)m * m) return;
+  const int i0 = (int)(id / m), i1 = (int)(id - (long long)i0 * m);
+  const int h = (m - 1) / 2;
+  const int d0 = i0 <= h ? i0 : i0 - m;
+  const int d1 = i1 <= h ? i1 : i1 - m;
+  const int jlo = -(nd / 2), jhi = (nd + 1) / 2 - 1;
+  double k = 0.0;
+  for (int a = 0; a < n_angles; ++a) k += dirichlet(d0 * cs[2 * a] + d1 * cs[2 * a + 1], nd, jlo, jhi);
+  out[id] = k;
+}
+
+int psf_kernel_grid(int m, const double* cs, int n_angles, int nd, double* out, cudaStream_t st) {
+  const int bs = 256;
+  const long long nb = ((long long)m * m + bs - 1) / bs;
+  k_psf_kernel_grid<<<(unsigned)nb, bs, 0, st>>>(out, m, cs, n_angles, nd);
+  return check_launch("k_psf_kernel_grid");
+}
+
 // PQ/Bi from the two spectra S[2][c][kx] (c = ky in [0, M/2])
 __global__ void k_psf_finish(const c32* __restrict__ spec, c32* __restrict__ PQ,
                              float* __restrict__ Bi, int n, int M, int flip) {

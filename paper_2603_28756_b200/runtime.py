@@ -310,17 +310,17 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
                 full = comm.gather(slab, parts)
                 if rank == 0:
                     snapshot_sink(k, full.to("cpu", torch.float64).numpy())
+        # the reference's record sink sees every record (runtime.py:654-659)
         slab, records = _iterate(ctx, params, cfg, x0, stencil, L, comm=comm,
                                  on_record=on_record if rank == 0 else None,
-                                 device_snapshot=sink)
+                                 device_snapshot=sink, x0_owned=True, log_filter=False)
         if gather == "none":
             return slab, records
         full = comm.gather(slab, parts)
         vol = Volume._owned(_device.to_host64(full)) if rank == 0 else None
         return vol, records
-    except (TransportError, ValueError, FloatingPointError):
-        raise
-    except Exception as exc:  # noqa: BLE001 - same contract as runtime.py:688-690
+    except Exception as exc:  # noqa: BLE001 - any worker failure, divergence included,
+        # surfaces as RuntimeError("worker i failed: ...") (runtime.py:684-690)
         raise RuntimeError(f"worker {rank} failed: {exc}") from exc
 
 
@@ -400,7 +400,8 @@ def distributed_solve_hierarchical(full_sino: Sinogram, hierarchy, params, cfg: 
         sink = ((lambda rec, _l=lvl: on_record(_l, rec))
                 if (on_record is not None and rank == 0) else None)
         stencil = stencil_3d() if n_z > 1 else stencil_2d()
-        estimate, records = _iterate(ctx, params, cfg_l, x0, stencil, L, comm=comm, on_record=sink)
+        estimate, records = _iterate(ctx, params, cfg_l, x0, stencil, L, comm=comm, on_record=sink,
+                                     x0_owned=True, log_filter=False)
         all_records.append(records)
         parts_prev = parts
     if gather == "none":

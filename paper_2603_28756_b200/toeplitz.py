@@ -13,6 +13,7 @@ M >= 2N-1 and runs the fused real-FFT convolution of csrc/toeplitz.cu
 from __future__ import annotations
 
 import collections
+import functools
 import math
 import os
 from dataclasses import dataclass, field
@@ -69,7 +70,14 @@ def fft_side_for(source_side: int) -> int:
 
 @dataclass(frozen=True)
 class PsfKernel:
-    """Device-resident spectra of the projection normal operator.
+    """Fourier-domain kernel of the projection normal operator (toeplitz.py:63-82).
+
+    Reference fields keep their meaning: ``padded_side`` is the reference's odd
+    7-smooth side m >= 2N-1 (``padded_side_for``), ``embed_offset`` = (m - N) // 2
+    and ``spectrum`` the fp64 (m, m) fft2 of the ifftshifted lag kernel -- computed
+    on first access (closed-form fp64 kernel on the device, fp64 FFT, read-only
+    host array).  The apply path uses the device spectra on the even grid
+    ``fft_side`` = M:
 
     ``pq``: (M/2+1, M, 2) fp32 = ((A + Re B)/M^2, (A - Re B)/M^2) with ``A`` the
     spectrum of (K - K_nyq)/Nd and ``B`` that of the flip kernel -K_nyq/Nd times
@@ -83,14 +91,32 @@ class PsfKernel:
     pq: torch.Tensor = field(repr=False)
     bi: torch.Tensor = field(repr=False)
     has_flip: bool = False
+    fft_side: int = 0
+    angles: np.ndarray = field(default=None, repr=False, compare=False, hash=False)
 
     @property
     def embed_offset(self) -> int:
-        return 0
+        return (self.padded_side - self.source_side) // 2
 
     @property
     def device(self) -> torch.device:
         return self.pq.device
+
+    @functools.cached_property
+    def spectrum(self) -> np.ndarray:
+        """fft2(ifftshift(K)) on the odd m x m grid, K(d) = sum_theta sum_j
+        cos(w_j d.e_theta) (toeplitz.py:102-103); read-only complex128."""
+        lib = _lib.ensure_ready()
+        m = self.padded_side
+        cs = np.stack([np.cos(self.angles), np.sin(self.angles)], axis=1)
+        d_cs = torch.from_numpy(np.ascontiguousarray(cs, dtype=np.float64)).to(self.device)
+        k = torch.empty((m, m), dtype=torch.float64, device=self.device)
+        _lib.check(lib.tf_psf_kernel(m, int(self.angles.size), d_cs.data_ptr(),
+                                     int(self.radial_count), k.data_ptr(), _lib.stream_handle()),
+                   "tf_psf_kernel")
+        spec = torch.fft.fft2(k).cpu().numpy()  # one-time fp64 library FFT (not the apply path)
+        spec.setflags(write=False)
+        return spec
 
 
 def _check_tolerance(tolerance: float, oversampling: float) -> None:
@@ -115,17 +141,18 @@ def clear_caches() -> None:
     nufft._TABLE_CACHE.clear()
 
 
-def _build(angles: np.ndarray, nd: int, source_side: int) -> PsfKernel:
+def _build(angles: np.ndarray, nd: int, source_side: int, odd_side: int | None = None) -> PsfKernel:
     """The kernel of a geometry; immutable, so kernels of the same geometry (repeated
     reconstructions, the levels of repeated hierarchical solves) are shared."""
     n = int(source_side)
     if n < 1:
         raise ValueError("source side must be positive")
     dev = _lib.device()
-    key = (dev.index, n, int(nd), np.asarray(angles, dtype=np.float64).tobytes())
+    odd = int(odd_side) if odd_side is not None else padded_side_for(n)
+    key = (dev.index, n, int(nd), odd, np.asarray(angles, dtype=np.float64).tobytes())
     psf = _PSF_CACHE.get(key)
     if psf is None:
-        psf = _PSF_CACHE[key] = _build_new(angles, nd, n, dev)
+        psf = _PSF_CACHE[key] = _build_new(angles, nd, n, dev, odd)
         while len(_PSF_CACHE) > _PSF_CACHE_SIZE:
             _PSF_CACHE.popitem(last=False)
     else:
@@ -133,7 +160,7 @@ def _build(angles: np.ndarray, nd: int, source_side: int) -> PsfKernel:
     return psf
 
 
-def _build_new(angles: np.ndarray, nd: int, n: int, dev) -> PsfKernel:
+def _build_new(angles: np.ndarray, nd: int, n: int, dev, odd: int) -> PsfKernel:
     lib = _lib.ensure_ready()
     m = fft_side_for(n)
     cs = np.stack([np.cos(angles), np.sin(angles)], axis=1).astype(np.float64)
@@ -148,8 +175,10 @@ def _build_new(angles: np.ndarray, nd: int, n: int, dev) -> PsfKernel:
                          bi.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_handle()),
         "tf_psf_build",
     )
-    return PsfKernel(padded_side=m, source_side=n, radial_count=int(nd), pq=pq, bi=bi,
-                     has_flip=(nd % 2 == 0))
+    ang = np.array(angles, dtype=np.float64)
+    ang.setflags(write=False)
+    return PsfKernel(padded_side=odd, source_side=n, radial_count=int(nd), pq=pq, bi=bi,
+                     has_flip=(nd % 2 == 0), fft_side=m, angles=ang)
 
 
 def compute_psf(plan_pad, source_side: int) -> PsfKernel:
@@ -164,7 +193,7 @@ def compute_psf(plan_pad, source_side: int) -> PsfKernel:
     if m % 2 == 0:
         raise ValueError("padded grid side must be odd so kernel lags are integers")
     s = plan_pad.sampling
-    return _build(np.asarray(s.angles), s.radial_count, source_side)
+    return _build(np.asarray(s.angles), s.radial_count, source_side, odd_side=m)
 
 
 def build_psf(sampling: PolarSampling, source_side: int, tolerance: float = 1e-6,
@@ -179,7 +208,7 @@ def apply_stack(psf: PsfKernel, x: torch.Tensor, out: torch.Tensor | None = None
                 beta: float = 0.0) -> torch.Tensor:
     """out = alpha * K x + beta * aux on a contiguous fp32 device stack (Z, N, N)."""
     lib = _lib.ensure_ready()
-    n, m = psf.source_side, psf.padded_side
+    n, m = psf.source_side, psf.fft_side
     if x.dim() != 3 or x.shape[1] != n or x.shape[2] != n:
         raise ValueError(f"image side {x.shape[-1]} does not match kernel source side {n}")
     if not x.is_contiguous() or x.dtype != torch.float32:
@@ -221,21 +250,41 @@ def toeplitz_apply(psf: PsfKernel, f):
     return _device.wrap_like(kind, apply_stack(psf, x))
 
 
-@dataclass(frozen=True)
 class FidelityContext:
-    """Per-(geometry, data) precomputation (toeplitz.py:173-197).
+    """Per-(geometry, data) precomputation reused across iterations (toeplitz.py:173-197).
 
-    ``rstar`` is the device (Z, N, N) fp32 adjoint R*g; ``rstar_g`` materialises
-    the reference's host ImageGrid/Volume view on demand.
+    Constructed as the reference does, ``FidelityContext(psf, rstar_g, g_norm_sq)``
+    with ``rstar_g`` an ImageGrid / Volume (or float64 array); it is uploaded once
+    and kept on the device as the fp32 (Z, N, N) stack ``rstar``.  Internal callers
+    pass the device stack directly (``rstar_g`` may be a CUDA tensor, or use the
+    ``rstar=`` keyword).  ``rstar_g`` returns the reference's host view (the
+    object given, or one materialised on demand).  Immutable.
     """
 
-    psf: PsfKernel
-    rstar: torch.Tensor = field(repr=False)
-    g_norm_sq: float
+    __slots__ = ("psf", "rstar", "g_norm_sq", "_host")
 
-    def __post_init__(self):
-        if self.rstar.shape[-1] != self.psf.source_side:
+    def __init__(self, psf: PsfKernel, rstar_g=None, g_norm_sq: float = 0.0, *, rstar=None):
+        if (rstar_g is None) == (rstar is None):
+            raise TypeError("FidelityContext needs exactly one of rstar_g / rstar")
+        src = rstar_g if rstar_g is not None else rstar
+        host = src if isinstance(src, (ImageGrid, Volume)) else None
+        if isinstance(src, torch.Tensor) and src.is_cuda:
+            dev = src.to(torch.float32)
+            dev = (dev[None] if dev.dim() == 2 else dev).contiguous()
+        else:
+            dev, _ = _device.as_stack(src, "rstar_g")
+        if dev.shape[-1] != psf.source_side:
             raise ValueError("adjoint image side does not match PSF source side")
+        for name, val in (("psf", psf), ("rstar", dev), ("g_norm_sq", float(g_norm_sq)),
+                          ("_host", host)):
+            object.__setattr__(self, name, val)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("FidelityContext is immutable")
+
+    def __repr__(self):
+        return (f"FidelityContext(psf=<N={self.psf.source_side}>, slices={self.slices}, "
+                f"g_norm_sq={self.g_norm_sq!r})")
 
     @property
     def slices(self) -> int:
@@ -247,6 +296,8 @@ class FidelityContext:
 
     @property
     def rstar_g(self):
+        if self._host is not None:
+            return self._host
         host = self.rstar.detach().to("cpu", torch.float64).numpy()
         return ImageGrid(host[0]) if host.shape[0] == 1 else Volume(host)
 
@@ -262,7 +313,7 @@ def fidelity_context(recon_plan, psf: PsfKernel, sino: Sinogram) -> FidelityCont
     if recon_plan.grid_side != psf.source_side:
         raise ValueError("reconstruction plan side does not match PSF source side")
     rstar = back_project_stack(recon_plan, sino.data)
-    return FidelityContext(psf=psf, rstar=rstar, g_norm_sq=float(np.sum(sino.data ** 2)))
+    return FidelityContext(psf, rstar=rstar, g_norm_sq=float(np.sum(sino.data ** 2)))
 
 
 def _fidelity_stack(ctx: FidelityContext, f):

@@ -104,3 +104,27 @@ def hier_worker(rank, world, port, fixture, out_dir):
                      "obj1": np.array([r.objective for r in lrecs[1]])}, allow_pickle=True)
     finally:
         dist.destroy_process_group()
+
+
+def diverge_worker(rank, world, port, fixture, out_dir):
+    """distributed_solve with a far too small Lipschitz constant: must raise
+    RuntimeError('worker <rank> failed: ...') wrapping the FloatingPointError."""
+    import paper_2603_28756_b200 as tf
+    from paper_2603_28756_b200.runtime import distributed_solve
+
+    torch.cuda.set_device(0)
+    _init(rank, world, port)
+    try:
+        d = dict(np.load(fixture))
+        sino = tf.Sinogram(angles=d["angles"], data=d["g"])
+        prm = tf.QggmrfParams(sigma=0.3, lam=0.05)
+        cfg = tf.SolverConfig(max_iters=500, tol=1e-300, lipschitz=1e-6, restart=False)
+        try:
+            distributed_solve(sino, 16, prm, cfg, world)
+            msg = "no error"
+        except Exception as exc:  # noqa: BLE001 - recorded for the test
+            msg = f"{type(exc).__name__}: {exc}"
+        with open(os.path.join(out_dir, f"diverge{rank}.txt"), "w") as fh:
+            fh.write(msg)
+    finally:
+        dist.destroy_process_group()

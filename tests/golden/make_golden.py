@@ -210,6 +210,121 @@ def c2_reduced():
     print("c2_reduced.npz written")
 
 
+SUBSET = 1 << 18  # voxels kept of the large reconstructions (seeded uniform sample)
+
+
+def _subset(vol: np.ndarray, seed: int) -> dict:
+    """A fixed uniform sample of a large volume plus size-independent summaries:
+    the relative L2 over 2^18 seeded voxels estimates the full-volume one."""
+    flat = vol.reshape(-1)
+    idx = np.sort(np.random.default_rng(seed).choice(flat.size, size=min(SUBSET, flat.size),
+                                                     replace=False)).astype(np.int64)
+    return {"idx": idx, "vals": flat[idx], "slice_norms": np.linalg.norm(vol, axis=(-2, -1)),
+            "total_sum": float(vol.sum())}
+
+
+def c2_full():
+    """C2 (configs[1]) at its stated size: 16 x 512^2 3-D Shepp-Logan, 90 sparse angles,
+    Nd = 1024, Poisson counts (I0 = 1e4, mu = 2.5 / max(g), seed 0),
+    qGGMRF lam = 5e-4, sigma = 0.1 range(FBP) ("auto", cli.py:90-98), L by the
+    reference's power iteration, 50 iterations, FBP init (solver.py:112-180).
+
+    The sinogram is rounded to float32 BEFORE the reference runs, so the GPU test
+    (which stores it as float32) sees bit-identical inputs."""
+    sys.path.insert(0, str(REF))
+    import tomoforge as tf
+    from tomoforge import solver
+
+    side, n_ang, bins, z = 512, 90, 1024, 16
+    ang = np.linspace(0.0, np.pi, n_ang, endpoint=False)
+    geom = tf.ScanGeometry(angles=ang, detector_bins=bins, image_side=side)
+    samp = tf.polar_sampling(geom)
+    plan = tf.NufftPlan(side, samp, 1e-6)
+    psf = tf.build_psf(samp, side, 1e-6)
+    truth = tf.shepp_logan(side, three_d=True, slices=z)
+    clean = tf.project_volume(plan, truth).data
+    i0, mu = 1e4, 2.5 / clean.max()
+    counts = np.random.default_rng(0).poisson(i0 * np.exp(-mu * clean))
+    g = (-np.log(np.maximum(counts, 1) / i0) / mu).astype(np.float32)
+    sino = tf.Sinogram(angles=ang, data=g.astype(np.float64))
+    ctx = tf.fidelity_context(plan, psf, sino)
+    f0 = tf.fbp(plan, sino)
+    sigma = 0.1 * float(f0.data.max() - f0.data.min())
+    prm = tf.QggmrfParams(sigma=sigma, lam=5e-4)
+    L = solver.estimate_lipschitz(psf, prm)
+    rec, recs = tf.solve(ctx, prm, tf.SolverConfig(max_iters=50, tol=1e-300, lipschitz=L), f0)
+    rs, fs = _subset(rec.data, 502), _subset(f0.data, 502)
+    np.savez_compressed(OUT / "c2_full.npz", angles=ang, g=g, sigma=sigma, L=L,
+                        recon_idx=rs["idx"], recon_vals=rs["vals"],
+                        recon_slice_norms=rs["slice_norms"], recon_sum=rs["total_sum"],
+                        f0_vals=fs["vals"], f0_slice_norms=fs["slice_norms"],
+                        objective=np.array([r.objective for r in recs]),
+                        restarted=np.array([r.restarted for r in recs]))
+    print("c2_full.npz written")
+
+
+def c3_chain():
+    """C3 (configs[2]) geometry at its stated finest size: a slab of 8 of the 64 slices of
+    the 2048^2 3-D Shepp-Logan (slices 28..35), 128 angles, Nd = 2048, the 3-level
+    (512, 1024, 2048) Lanczos-3 schedule of multires.solve_hierarchical
+    (multires.py:198-242) with FBP init and a reduced iteration budget (6, 3, 2).  The
+    Lipschitz constant is left to the reference's per-level power iteration
+    (cfg.lipschitz = None); the estimates are logged.  Slab z-downsampling gives
+    2 -> 4 -> 8 slices over the levels (multires.py:123-124)."""
+    sys.path.insert(0, str(REF))
+    import time
+
+    import tomoforge as tf
+    from tomoforge import geometry, multires, solver
+
+    side, n_ang, bins, z_total, z0, z = 2048, 128, 2048, 64, 28, 8
+    ang = np.linspace(0.0, np.pi, n_ang, endpoint=False)
+    geom = tf.ScanGeometry(angles=ang, detector_bins=bins, image_side=side)
+    samp = tf.polar_sampling(geom)
+    plan = tf.NufftPlan(side, samp, 1e-6)
+    t0 = time.time()
+    # the slab's slices of shepp_logan(2048, three_d=True, slices=64) (geometry.py:254-271)
+    truth = np.zeros((z, side, side))
+    for k in range(z):
+        iz = z0 + k
+        zc = (2.0 * iz - z_total + 1.0) / z_total
+        scale = np.sqrt(max(0.0, 1.0 - (zc / geometry._Z_ENVELOPE) ** 2))
+        truth[k] = geometry._rasterize_ellipses(side, axis_scale=scale)
+    clean = tf.project_volume(plan, tf.Volume(truth)).data
+    g = (clean + 0.5 * np.random.default_rng(33).standard_normal(clean.shape)).astype(np.float32)
+    sino = tf.Sinogram(angles=ang, data=g.astype(np.float64))
+    f_fbp = tf.fbp(plan, sino)
+    sigma = 0.1 * float(f_fbp.data.max() - f_fbp.data.min())  # sigma "auto" (cli.py:90-98)
+    print(f"c3: sinogram + fbp {time.time() - t0:.0f}s", flush=True)
+    prm = tf.QggmrfParams(sigma=sigma, lam=5e-4)
+    lips = []
+    orig = solver.estimate_lipschitz
+
+    def logged(psf, params):
+        v = orig(psf, params)
+        lips.append(v)
+        return v
+
+    solver.estimate_lipschitz = logged
+    try:
+        hier = multires.GridHierarchy(levels=(512, 1024, 2048), iters_per_level=(6, 3, 2))
+        est, lrecs = multires.solve_hierarchical(sino, hier, prm,
+                                                 tf.SolverConfig(max_iters=1, tol=1e-300),
+                                                 use_fbp_init=True)
+    finally:
+        solver.estimate_lipschitz = orig
+    print(f"c3: solve_hierarchical done {time.time() - t0:.0f}s", flush=True)
+    rs = _subset(est.data, 503)
+    np.savez_compressed(
+        OUT / "c3_chain.npz", angles=ang, g=g, sigma=sigma, lipschitz=np.array(lips),
+        iters=np.array(hier.iters_per_level), levels=np.array(hier.levels),
+        recon_idx=rs["idx"], recon_vals=rs["vals"], recon_slice_norms=rs["slice_norms"],
+        recon_sum=rs["total_sum"],
+        **{f"objective{i}": np.array([r.objective for r in recs]) for i, recs in enumerate(lrecs)},
+        **{f"restarted{i}": np.array([r.restarted for r in recs]) for i, recs in enumerate(lrecs)})
+    print("c3_chain.npz written")
+
+
 def fileio_fixtures():
     """Files written by the reference's fileio (tests/golden/fileio/): raw arrays with
     sidecars, a plan and its parse, a convergence CSV and a PGM preview."""
@@ -250,6 +365,10 @@ if __name__ == "__main__":
         c2_reduced()
     elif "--only-fileio" in sys.argv:
         fileio_fixtures()
+    elif "--only-c2-full" in sys.argv:
+        c2_full()
+    elif "--only-c3" in sys.argv:
+        c3_chain()
     else:
         main()
         c2_reduced()

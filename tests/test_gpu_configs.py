@@ -48,6 +48,70 @@ def test_c2_reduced_poisson(tf):
                                atol=1e-4 * abs(d["objective"][0]))
 
 
+def _subset_err(vol, d, prefix="recon"):
+    """relative L2 over the fixture's 2^18 seeded voxels, and over per-slice norms"""
+    flat = np.asarray(vol).reshape(-1)
+    return (rel_l2(flat[d["recon_idx"]], d[f"{prefix}_vals"]),
+            rel_l2(np.linalg.norm(np.asarray(vol), axis=(-2, -1)), d[f"{prefix}_slice_norms"]))
+
+
+def test_c2_stated_size(tf):
+    """C2 at its stated size (configs[1]): 16 x 512^2 3-D Shepp-Logan, 90 angles,
+    Nd = 1024, Poisson counts, sigma = 0.1 range(FBP), 50 iterations from FBP, vs
+    the reference run (tests/golden/make_golden.py c2_full; same float32 sinogram)."""
+    d = golden("c2_full.npz")
+    g = d["g"].astype(np.float64)
+    n = 512
+    p = _plan(tf, d["angles"], g.shape[2], n)
+    sino = tf.Sinogram(angles=d["angles"], data=g)
+    f0 = tf.fbp(p, sino)
+    fl = f0.data.reshape(-1)
+    assert rel_l2(fl[d["recon_idx"]], d["f0_vals"]) < 1e-5
+    assert 0.1 * float(f0.data.max() - f0.data.min()) == pytest.approx(float(d["sigma"]), rel=1e-4)
+    ctx = tf.fidelity_context(p, tf.build_psf(p.sampling, n), sino)
+    prm = tf.QggmrfParams(sigma=float(d["sigma"]), lam=5e-4)
+    rec, recs = tf.solve(ctx, prm, tf.SolverConfig(max_iters=50, tol=1e-300,
+                                                   lipschitz=float(d["L"])), f0)
+    err, err_norms = _subset_err(rec.data, d)
+    assert err < 1e-3 and err_norms < 1e-3  # reconstruction gate (north star)
+    assert [r.restarted for r in recs] == list(d["restarted"])
+    np.testing.assert_allclose([r.objective for r in recs], d["objective"], rtol=1e-4,
+                               atol=1e-4 * abs(d["objective"][0]))
+    L = tf.estimate_lipschitz(ctx.psf, prm)
+    assert L == pytest.approx(float(d["L"]), rel=1e-3)
+
+
+def test_c3_chain_stated_size(tf):
+    """C3 geometry at its stated finest size (configs[2]): an 8-slice 2048^2 slab of the
+    64-slice phantom, 128 angles, Nd = 2048, levels (512, 1024, 2048) with Lanczos-3
+    transfer, FBP init, per-level power-iteration Lipschitz constants, iterations
+    (6, 3, 2), vs the reference's solve_hierarchical (multires.py:198-242); this also
+    covers the full K4/K5 tile grid and the solver at 2048^2."""
+    d = golden("c3_chain.npz")
+    g = d["g"].astype(np.float64)
+    sino = tf.Sinogram(angles=d["angles"], data=g)
+    hier = tf.GridHierarchy(levels=tuple(int(v) for v in d["levels"]),
+                            iters_per_level=tuple(int(v) for v in d["iters"]))
+    prm = tf.QggmrfParams(sigma=float(d["sigma"]), lam=5e-4)
+    est, lrecs = tf.solve_hierarchical(sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300),
+                                       use_fbp_init=True)
+    assert est.data.shape == (8, 2048, 2048)
+    err, err_norms = _subset_err(est.data, d)
+    assert err < 1e-3 and err_norms < 1e-3
+    for lvl, recs in enumerate(lrecs):
+        assert [r.restarted for r in recs] == list(d[f"restarted{lvl}"])
+        np.testing.assert_allclose([r.objective for r in recs], d[f"objective{lvl}"], rtol=1e-4)
+    # the per-level Lipschitz estimates the reference used
+    from paper_2603_28756_b200.multires import _strided_indices
+
+    for lvl, side in enumerate(hier.levels):
+        f = 1 << (len(hier.levels) - 1 - lvl)
+        nd = _strided_indices(g.shape[2], f).size
+        geom = tf.ScanGeometry(angles=d["angles"], detector_bins=nd, image_side=side)
+        L = tf.estimate_lipschitz(tf.build_psf(tf.polar_sampling(geom), side), prm)
+        assert L == pytest.approx(float(d["lipschitz"][lvl]), rel=1e-3)
+
+
 @pytest.mark.parametrize("n", [640, 1280])
 def test_wedge_apply_vs_oracle(tf, n):
     """C5 geometry: 120 angles uniform in [0, 2 pi / 3) (limited-angle wedge), Nd = N."""
@@ -71,7 +135,7 @@ def test_large_sides_operator_properties(tf, n):
     ang = np.linspace(0.0, np.pi, 64, endpoint=False)
     geom = tf.ScanGeometry(angles=ang, detector_bins=n, image_side=n)
     psf = tf.build_psf(tf.polar_sampling(geom), n)
-    assert psf.padded_side == 8192
+    assert psf.fft_side == 8192
     gen = torch.Generator(device="cuda").manual_seed(n)
     x = torch.randn((1, n, n), device="cuda", generator=gen, dtype=torch.float32)
     y = torch.randn((1, n, n), device="cuda", generator=gen, dtype=torch.float32)

@@ -79,3 +79,21 @@ def test_hierarchical_over_slabs_matches_reference(tf, tmp_path):
     assert rel_l2(r["vol"], d["recon"]) < 1e-3
     np.testing.assert_allclose(r["obj0"], d["obj0"], rtol=1e-4)
     np.testing.assert_allclose(r["obj1"], d["obj1"], rtol=1e-4)
+
+
+def test_worker_divergence_is_runtime_error(tf, tmp_path):
+    """A diverging slab solve surfaces as RuntimeError('worker i failed ...') on every
+    rank, as the reference's threads do (runtime.py:684-690; its
+    test_worker_failure_propagates)."""
+    import torch.multiprocessing as mp
+
+    from _dist_workers import diverge_worker
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(diverge_worker, args=(2, port, str(GOLDEN / "runtime.npz"), str(tmp_path)),
+             nprocs=2, join=True)
+    for rank in range(2):
+        msg = (tmp_path / f"diverge{rank}.txt").read_text()
+        assert msg.startswith("RuntimeError") and "worker" in msg and "non-finite" in msg

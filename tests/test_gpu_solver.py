@@ -226,9 +226,12 @@ def test_device_decision_matches_host_arithmetic(tf, rng):
     obj, fid, prior, t = 10.0, 9.0, 2.7, 1.0
     cases = [(rng.standard_normal(), abs(rng.standard_normal()), rng.standard_normal() * 1e-3)
              for _ in range(40)]
-    cases += [(prior, 1.0, 0.0), (float("inf"), 1.0, -1.0)]  # dobj = 0 -> converged; inf
+    # None: e_new = the CURRENT prior and dfid = 0, i.e. dobj = 0 -> converged; then inf
+    cases += [None, (float("inf"), 1.0, -1.0)]
+    n_conv = 0
     for restart in (True, False):
-        for e_new, gsq, dfid in cases:
+        for case in cases:
+            e_new, gsq, dfid = (prior, 1.0, 0.0) if case is None else case
             vals = torch.tensor([e_new, gsq, dfid], dtype=torch.float64, device="cuda")
             rec = torch.empty(8, dtype=torch.float64, device="cuda")
             solver_decide(vals, state, c_dev, rec, lam=lam, with_prior=True, restart=restart,
@@ -245,8 +248,75 @@ def test_device_decision_matches_host_arithmetic(tf, rng):
             assert r[1] == fid + dfid and r[3] == gsq and r[7] == dobj or not fin
             assert bool(r[4]) == rst and bool(r[5]) == conv and bool(r[6]) == fin
             assert float(c_dev.item()) == float(np.float32(c_next)) or not fin
+            n_conv += int(r[5])
+            if case is None:
+                assert r[7] == 0.0 and bool(r[5]), "zero increment must converge"
             if not fin:  # the solver raises here; restart the synthetic sequence
                 state.copy_(torch.tensor([10.0, 9.0, 2.7, 1.0, 0.0], dtype=torch.float64))
                 obj, fid, prior, t = 10.0, 9.0, 2.7, 1.0
                 continue
             obj, fid, prior, t = obj_new, fid + dfid, e_new, t_next
+    assert n_conv >= 2
+
+
+def test_early_stop_records_and_snapshots(tf):
+    """A realistic tolerance stops the solve early: the returned iterate, the records
+    and the snapshots (k = 1 .. k_stop, no look-ahead iterate) agree with a fixed
+    schedule of exactly k_stop iterations (solver.py:170-178)."""
+    d = golden("solve_2d.npz")
+    n = d["f0"].shape[1]
+    ctx = _ctx(tf, d["angles"], d["g"], n)
+    prm = tf.QggmrfParams(sigma=float(d["sigma"]), lam=float(d["lam"]))
+    # a tolerance the fixed 30-iteration run crosses between iterations 5 and 20
+    _, probe = tf.solve(ctx, prm, tf.SolverConfig(max_iters=30, tol=1e-300,
+                                                  lipschitz=float(d["L"])), d["f0"][0])
+    ratios = [abs(b.objective - a.objective) / abs(a.objective)
+              for a, b in zip(probe, probe[1:]) if not b.restarted]
+    tol = 1.5 * min(ratios[5:20])
+    snaps = []
+    cfg = tf.SolverConfig(max_iters=400, tol=tol, lipschitz=float(d["L"]))
+    rec, recs = tf.solve(ctx, prm, cfg, d["f0"][0], snapshot_sink=lambda k, s: snaps.append((k, s)))
+    k_stop = recs[-1].iter
+    assert 1 < k_stop <= 21, "tolerance should stop the solve early"
+    assert [r.iter for r in recs] == list(range(k_stop + 1))
+    last = recs[-1]
+    assert not last.restarted and abs(last.objective - recs[-2].objective) <= tol * abs(
+        recs[-2].objective)
+    assert [k for k, _ in snaps] == list(range(1, k_stop + 1))
+    np.testing.assert_array_equal(snaps[-1][1], rec)
+    fixed, frecs = tf.solve(ctx, prm, tf.SolverConfig(max_iters=k_stop, tol=1e-300,
+                                                      lipschitz=float(d["L"])), d["f0"][0])
+    np.testing.assert_array_equal(fixed, rec)
+    assert [r.objective for r in frecs] == [r.objective for r in recs]
+
+
+def test_divergence_sends_no_nonfinite_snapshot(tf):
+    d = golden("solve_2d.npz")
+    n = d["f0"].shape[1]
+    ctx = _ctx(tf, d["angles"], d["g"], n)
+    prm = tf.QggmrfParams(sigma=float(d["sigma"]), lam=float(d["lam"]))
+    snaps = []
+    with pytest.raises(FloatingPointError):
+        tf.solve(ctx, prm, tf.SolverConfig(max_iters=400, tol=1e-300, lipschitz=1e-6,
+                                           restart=False),
+                 d["f0"][0], snapshot_sink=lambda k, s: snaps.append((k, s)))
+    assert snaps and all(np.all(np.isfinite(s)) for _, s in snaps)
+    assert [k for k, _ in snaps] == list(range(1, len(snaps) + 1))
+
+
+def test_cuda_input_is_not_modified(tf):
+    """solve copies a caller-owned CUDA f0 (solver.py:121); host inputs are converted
+    into a buffer the loop owns."""
+    import torch
+
+    d = golden("solve_3d.npz")
+    n = d["f0"].shape[1]
+    ctx = _ctx(tf, d["angles"], d["g"], n)
+    prm = tf.QggmrfParams(sigma=float(d["sigma"]), lam=float(d["lam"]))
+    cfg = tf.SolverConfig(max_iters=5, tol=1e-300, lipschitz=float(d["L"]))
+    f0 = torch.from_numpy(d["f0"].astype(np.float32)).cuda()
+    keep = f0.clone()
+    out, _ = tf.solve(ctx, prm, cfg, f0)
+    assert torch.equal(f0, keep)
+    host, _ = tf.solve(ctx, prm, cfg, d["f0"])
+    np.testing.assert_array_equal(out.cpu().numpy().astype(np.float64), host)
