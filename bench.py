@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-mbir", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--c4-side", type=int, default=2048, help="C4 volume side (2048 = configs[3])")
     return ap.parse_args()
 
 
@@ -233,6 +235,8 @@ def run_ours(args, world, rank, local):
     from paper_2603_28756_b200.toeplitz import apply_stack
 
     dev = torch.device("cuda", torch.cuda.current_device())
+    # C4 first, on a clean device (R*g + 4 volumes of 2048^3 take ~175 of 191 GB)
+    c4 = None if args.no_c4 else _c4(args, world, rank)
     z = args.slices
     geom = tf.ScanGeometry(angles=angles(), detector_bins=N_BINS, image_side=N_SIDE)
     psf = tf.build_psf(tf.polar_sampling(geom), N_SIDE)
@@ -314,7 +318,7 @@ def run_ours(args, world, rank, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: randn volume, R*g from a randn sinogram",
             "config": config(args, world), "roofline": roofline, "cpu_baseline": cpu,
-            "e2e": e2e, "gpu_launches": launches, "mbir": mbir,
+            "e2e": e2e, "gpu_launches": launches, "mbir": mbir, "mbir_c4": c4,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -507,6 +511,98 @@ def _mbir_distributed(tf, z, world, rank, prm, L, timed, setup, per_it_local, bp
         "solve_bytes_per_voxel_iter": bpv,
         "solve_hbm_frac": bpv * z * N_SIDE * N_SIDE / (step_ms / 1e3) / 1e9 / peak,
         "comm_per_iter": "2 halo planes of 16.8 MB per interior boundary + one 3 x fp64 allreduce",
+    }
+
+
+def _c4(args, world, rank):
+    """configs[3] (C4), the metric's second half: a side^3 volume (2048^3) reconstructed
+    end to end -- sinogram upload, FBP init at the coarsest level, the 3-level
+    (side/4, side/2, side) x (40, 20, 10) Lanczos schedule with per-level power-iteration
+    Lipschitz constants (multires.py:198-242) -- on ``world`` GPUs (z-slabs, NCCL halo
+    + scalar allreduce for world > 1).  Data: the 3-D Shepp-Logan phantom projected by
+    the GPU forward projector (128 angles, Nd = side) plus Gaussian noise; the
+    synthesis is not timed.  At W = 1 the solver holds R*g + 4 volumes (5 x 34.4 GB)."""
+    import torch
+
+    import paper_2603_28756_b200 as tf
+    from paper_2603_28756_b200.multires import solve_hierarchical_device
+    from paper_2603_28756_b200.phantoms import shepp_logan_slab
+    from paper_2603_28756_b200.radon import forward_project_stack
+
+    n = args.c4_side
+    nd = n
+    free, total = torch.cuda.mem_get_info()
+    need = 5 * 4 * n ** 3 / world + 12e9
+    if free < need:
+        return {"skipped": f"needs ~{need / 1e9:.0f} GB free per GPU, {free / 1e9:.0f} GB free"}
+    geom = tf.ScanGeometry(angles=angles(), detector_bins=nd, image_side=n)
+    plan = tf.NufftPlan(n, tf.polar_sampling(geom), 1e-6)
+    t0 = time.perf_counter()
+    rows = np.empty((n, N_ANGLES, nd), dtype=np.float32)
+    gen = torch.Generator(device="cuda").manual_seed(44)
+    chunk = 64
+    for z0 in range(0, n, chunk):
+        z1 = min(n, z0 + chunk)
+        r = forward_project_stack(plan, shepp_logan_slab(n, n, z0, z1))
+        r += 0.5 * torch.randn(r.shape, device=r.device, generator=gen)
+        rows[z0:z1] = r.cpu().numpy()
+    del r
+    sino = tf.Sinogram(angles=angles(), data=rows)
+    del rows
+    t_synth = time.perf_counter() - t0
+    tf.clear_caches()
+    torch.cuda.empty_cache()
+    hier = tf.GridHierarchy(levels=(n // 4, n // 2, n), iters_per_level=(40, 20, 10))
+    prm = tf.QggmrfParams(sigma=0.1, lam=5e-4)
+    cfg = tf.SolverConfig(max_iters=1, tol=1e-300)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.reset_peak_memory_stats()
+    t0 = time.perf_counter()
+    if world == 1:
+        est, lrecs = solve_hierarchical_device(sino, hier, prm, cfg, use_fbp_init=True)
+    else:
+        from paper_2603_28756_b200.runtime import distributed_solve_hierarchical
+
+        est, lrecs = distributed_solve_hierarchical(sino, hier, prm, cfg, world, use_fbp_init=True,
+                                                    gather="none")
+    torch.cuda.synchronize()
+    t_solve = max_over_ranks(time.perf_counter() - t0, world)
+    peak_gb = torch.cuda.max_memory_allocated() / 1e9
+    t0 = time.perf_counter()
+    out = np.empty(tuple(est.shape), dtype=np.float32)
+    step = 64
+    for z0 in range(0, est.shape[0], step):
+        out[z0:z0 + step] = est[z0:z0 + step].cpu().numpy()
+    t_d2h = max_over_ranks(time.perf_counter() - t0, world)
+    finite = bool(np.isfinite(out[::97]).all())
+    del out, est
+    torch.cuda.empty_cache()
+    peak = _peak_hbm()["value"]
+    per_level = []
+    for lvl, recs in enumerate(lrecs):
+        side = hier.levels[lvl]
+        steps = sorted(r.step_time for r in recs if r.iter >= 2)
+        ms = 1e3 * steps[len(steps) // 2] if steps else None
+        ms = max_over_ranks(ms, world) if ms is not None else None
+        vox = side ** 3 / world
+        per_level.append({"side": side, "slices": side, "iters": len(recs) - 1,
+                          "ms_per_iter_median": ms, "restarts": int(sum(r.restarted for r in recs)),
+                          "hbm_frac_at_88B": (88.0 * vox / (ms / 1e3) / 1e9 / peak) if ms else None})
+    return {
+        "config": f"C4: {n}^3 3-D Shepp-Logan, {N_ANGLES} angles, Nd={nd}, noise rms 0.5, "
+                  f"levels {hier.levels} x {hier.iters_per_level}, FBP init, qGGMRF sigma=0.1 "
+                  f"lam=5e-4, per-level power-iteration L, z-slabs over {world} GPU(s)",
+        "n_gpus": world,
+        "mbir_end_to_end_s": t_solve,
+        "mbir_end_to_end_note": "solve_hierarchical from the host float64 sinogram (upload, "
+                                "R*g/FBP per level, PSFs, Lipschitz estimates, all iterations, "
+                                "Lanczos transfers) to the finest estimate on the device",
+        "result_d2h_fp32_s": t_d2h,
+        "per_level": per_level,
+        "peak_device_gb": peak_gb,
+        "synthesis_s_untimed": t_synth,
+        "finite": finite,
     }
 
 

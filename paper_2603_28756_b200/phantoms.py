@@ -56,6 +56,32 @@ def shepp_logan(side: int, three_d: bool = False, slices: int = 1):
     return Volume(np.stack([_slice(side, float(s)) for s in scales]))
 
 
+def shepp_logan_slab(side: int, slices: int, z_begin: int, z_end: int, device=None):
+    """Slices [z_begin, z_end) of ``shepp_logan(side, three_d=True, slices=slices)``
+    evaluated on the device in float64 (same pixel centres, table and taper; returns
+    an fp32 (z_end - z_begin, side, side) tensor).  Input generator for volumes too
+    large for host numpy (C4: 2048^3)."""
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    zc = np.zeros(1) if slices == 1 else (2.0 * np.arange(slices) - (slices - 1.0)) / slices
+    scales = np.sqrt(np.maximum(0.0, 1.0 - (zc / _Z_EXTENT) ** 2))[z_begin:z_end]
+    c = torch.from_numpy((2.0 * np.arange(side) - (side - 1.0)) / side).to(dev)
+    gx, gy = c[:, None], c[None, :]
+    out = torch.zeros((z_end - z_begin, side, side), dtype=torch.float32, device=dev)
+    for k, sc in enumerate(scales):
+        if sc <= 0.0:
+            continue
+        img = torch.zeros((side, side), dtype=torch.float64, device=dev)
+        for val, a, b, x0, y0, deg in _TABLE:
+            cs, sn = np.cos(np.deg2rad(deg)), np.sin(np.deg2rad(deg))
+            u, v = gx - x0 * sc, gy - y0 * sc
+            inside = ((u * cs + v * sn) / (a * sc)) ** 2 + ((v * cs - u * sn) / (b * sc)) ** 2
+            img += torch.where(inside <= 1.0, val, 0.0)
+        out[k] = img.clamp_min_(0.0)
+    return out
+
+
 def disk_phantom(side: int, radius: float, value: float = 1.0):
     """``value`` at pixel centres strictly inside ``radius``, zero elsewhere."""
     from .geometry import ImageGrid
