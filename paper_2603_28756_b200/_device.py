@@ -68,12 +68,9 @@ def as_stack(f, what: str = "input"):
 
 
 _CHUNK_ELEMS = 1 << 25  # 256 MB of float64 per staged copy
-# host float64 inputs are narrowed to fp32 by the staging threads (TF_STAGE_F32=0:
-# stage float64 and narrow on the device); bit-identical either way
-_STAGE_F32 = os.environ.get("TF_STAGE_F32", "1") != "0"
-
-
-_STAGE_THREADS = int(os.environ.get("TF_STAGE_THREADS", min(8, os.cpu_count() or 1)))
+# host float64 inputs are narrowed to fp32 by the staging threads (round to
+# nearest, bit-identical to narrowing on the device, half the upload bytes)
+_STAGE_THREADS = min(8, os.cpu_count() or 1)
 _stage_pool = None
 
 
@@ -105,7 +102,7 @@ def to_device(arr: np.ndarray) -> torch.Tensor:
         return out
     chunk = _CHUNK_ELEMS
     # narrowed to fp32 by the host threads while staging (see pipelined_host_map)
-    tdt = torch.float64 if flat.dtype == np.float64 and not _STAGE_F32 else torch.float32
+    tdt = torch.float32
     stages = [torch.empty(chunk, dtype=tdt, pin_memory=True) for _ in range(2)]
     events = [None, None]
     stream = torch.cuda.current_stream()
@@ -226,7 +223,7 @@ def _wrap_host(kind: str, host: np.ndarray):
     return host
 
 
-_PIPE_SLICE_BYTES = int(os.environ.get("TF_PIPE_MB", 256)) << 20
+_PIPE_SLICE_BYTES = 256 << 20
 _streams: dict = {}
 
 
@@ -256,7 +253,7 @@ def pipelined_host_map(arr: np.ndarray, kind: str, fn):
         out = torch.empty(stack.shape, dtype=torch.float64)
     # the host threads narrow to fp32 while staging (round to nearest, as the device
     # conversion would): half the upload bytes and half the staging writes
-    sdt = torch.float32 if _STAGE_F32 else torch.float64
+    sdt = torch.float32
     stages = [torch.empty(step * plane, dtype=sdt, pin_memory=True) for _ in range(2)]
     staged = [None, None]
     caller = torch.cuda.current_stream()

@@ -7,6 +7,7 @@ Each ``csrc/*.cu`` is its own translation unit, compiled in parallel
 
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -36,17 +37,36 @@ def headers():
     return sorted(CSRC.glob("*.cuh"))
 
 
+def _digest(paths, extra=()) -> str:
+    """Content hash of sources + headers + flags: a stale library (or object) is
+    rebuilt whatever the file times say (snapshots copied to a GPU box keep or
+    reset mtimes arbitrarily)."""
+    h = hashlib.sha256()
+    for p in paths:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    for e in (*NVCC_FLAGS, *_DEFINES, *extra):
+        h.update(e.encode())
+    return h.hexdigest()
+
+
+def _stamp(path: Path) -> Path:
+    return path.with_name(path.name + ".sha256")
+
+
+def library_digest() -> str:
+    return _digest(units() + headers())
+
+
 def up_to_date() -> bool:
-    if not LIB.exists():
-        return False
-    t = LIB.stat().st_mtime
-    return all(p.stat().st_mtime <= t for p in units() + headers() + [Path(__file__)])
+    stamp = _stamp(LIB)
+    return LIB.exists() and stamp.exists() and stamp.read_text().strip() == library_digest()
 
 
 def _compile(nvcc: str, src: Path, verbose: bool):
     obj = OBJ / (src.stem + ".o")
-    newest_dep = max(p.stat().st_mtime for p in [src] + headers() + [Path(__file__)])
-    if obj.exists() and obj.stat().st_mtime >= newest_dep:
+    want = _digest([src] + headers())
+    if obj.exists() and _stamp(obj).exists() and _stamp(obj).read_text().strip() == want:
         return obj, None
     cmd = [nvcc, *NVCC_FLAGS, *_DEFINES, "-c", str(src), "-o", str(obj)]
     if verbose:
@@ -56,6 +76,7 @@ def _compile(nvcc: str, src: Path, verbose: bool):
         return obj, f"{src.name}: nvcc failed ({res.returncode})\n{res.stdout}{res.stderr}"
     if verbose:
         sys.stderr.write(res.stderr)
+    _stamp(obj).write_text(want)
     return obj, None
 
 
@@ -81,6 +102,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc link failed ({res.returncode})")
     os.replace(str(LIB) + ".tmp", LIB)
+    _stamp(LIB).write_text(library_digest())
     return LIB
 
 

@@ -1034,7 +1034,6 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
 #define TF_K4(TD, P2V, NN)                                                                    \
   k_prior_update<TD, P2V, NN><<<grid, TX * TY, 0, st>>>(F, FP, Kf, Kfp, rstar, f_new, partial, \
                                                          nz, h, w_, c, lam, inv_L, write_grad, pc, c_dev)
-  static const int sym = getenv("TF_K4_SYM") ? atoi(getenv("TF_K4_SYM")) : 1;
   const dim3 sgrid = sym_grid(h, w_);
   const size_t ssmem = sym_smem_bytes();
 #define TF_K4S(P2V, NN)                                                                      \
@@ -1043,12 +1042,10 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
     k_prior_update_sym<P2V, NN><<<sgrid, TX * TY, ssmem, st>>>(                              \
         F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, c, lam, inv_L, write_grad, pc, c_dev); \
   } while (0)
-  if (three_d && sym) {
+  // 3-D: the symmetric-clique tile kernel; 2-D (single slices): the direct stencil
+  if (three_d) {
     if (p2) { if (nonneg) TF_K4S(true, true); else TF_K4S(true, false); }
     else { if (nonneg) TF_K4S(false, true); else TF_K4S(false, false); }
-  } else if (three_d) {
-    if (p2) { if (nonneg) TF_K4(true, true, true); else TF_K4(true, true, false); }
-    else { if (nonneg) TF_K4(true, false, true); else TF_K4(true, false, false); }
   } else {
     if (p2) { if (nonneg) TF_K4(false, true, true); else TF_K4(false, true, false); }
     else { if (nonneg) TF_K4(false, false, true); else TF_K4(false, false, false); }
@@ -1056,7 +1053,7 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
 #undef TF_K4
 #undef TF_K4S
   TF_TRY(check_launch("k_prior_update"));
-  const int nparts = three_d && sym ? (int)(sgrid.x * sgrid.y) : (int)(grid.x * grid.y);
+  const int nparts = three_d ? (int)(sgrid.x * sgrid.y) : (int)(grid.x * grid.y);
   k_sum_partials<<<1, 1024, 0, st>>>(partial, nparts, 1, out_gsq);
   return check_launch("k_sum_partials");
 }
@@ -1069,8 +1066,7 @@ int energy_fid(const float* fn, const float* fn_hi, const float* f, const float*
   const dim3 grid = tile_grid(h, w_);
   const Planes FN{fn, nullptr, fn_hi};
   const bool p2 = p == 2.0;
-  static const int tiled = getenv("TF_K5_TILED") ? atoi(getenv("TF_K5_TILED")) : 1;
-  if (three_d && with_prior && tiled) {
+  if (three_d && with_prior) {  // 3-D energy on K4's tile geometry
     const dim3 sg = sym_grid(h, w_);
     if (p2) k_energy_fid_t<true><<<sg, TX * TY, 0, st>>>(FN, f, Kfn, Kf, rstar, partial, nz, h, w_, pc);
     else k_energy_fid_t<false><<<sg, TX * TY, 0, st>>>(FN, f, Kfn, Kf, rstar, partial, nz, h, w_, pc);

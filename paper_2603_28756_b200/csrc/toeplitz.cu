@@ -430,175 +430,19 @@ k_cols_conv(c32* __restrict__ T, const c32* __restrict__ PQ, const float* __rest
   }
 }
 
-// twiddle source for K2: the last pass (k = t for every butterfly) reads a
-// per-thread set precomputed once per kernel; earlier passes use the table
-template <int M, int E>
-struct TwLastCached {
-  using S = FftShape<M, E>;
-  const PassTw<M, E, S::NP - 1>* last;
-  template <int P>
-  __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
-    if constexpr (P == S::NP - 1) tw = *last;
-    else tw.from_table(t);
-  }
-};
-
-// Persistent, TMA-fed K2 for large M.  Each CTA walks its (column, slice-pair)
-// items: NB = 2 slices of one column share the PSF column in registers (and the
-// cached last-pass twiddles).  One thread keeps the next S items in flight:
-// TMA 4-D tensor copies (box = 32 B x BOXR row blocks) gather the column's
-// pieces from every row block into a contiguous shared buffer, completing on
-// the stage's `full` mbarrier.  A stage is refilled only after every thread has
-// arrived on its `empty` mbarrier (release/acquire ordering of the generic
-// reads before the async-proxy write; a bare __syncthreads is not enough since
-// BAR.SYNC lets the issuing warp run ahead).  Results are staged in shared
-// memory and written back in place by TMA tensor stores.
-// PP: ping-pong exchange buffers (one barrier per exchange) and direct stores
-// of the results (8-byte lanes, 32-byte sector-complete) instead of TMA stores.
-template <int M, int E, int S, bool FLIP, int NB, bool CACHE, bool PP>
-__global__ void __launch_bounds__(M / E, (NB == 1 && !CACHE) ? 2 : 1)
-k_cols_conv_tma(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ PQ,
-                const float* __restrict__ Bi, int ncols, int nrb, int nslices, int boxr,
-                c32* __restrict__ T) {
-  constexpr int TT = M / E;
-  constexpr int SB = group_stride(M, NB);
-  constexpr int CL = M / 2;  // column buffer words (>= nrb * 4)
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  // [out: NB*CL unless PP][stages: S*NB*CL][xbuf: NB*SB (x2 if PP)][full: S][empty: S]
-  c32* outb = reinterpret_cast<c32*>(smem_raw);
-  c32* inb = outb + (PP ? 0 : NB * CL);
-  c32* xbuf = inb + S * NB * CL;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + (PP ? 2 : 1) * NB * SB);
-  uint64_t* empty = full + S;
-  const int t = threadIdx.x;
-  if ((int)blockIdx.x >= ncols) return;
-  const int my_cols = (ncols - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int pairs = (nslices + NB - 1) / NB;  // items per column
-  const long long nitems = (long long)my_cols * pairs;
-  const int nbox = (nrb + boxr - 1) / boxr;
-  const uint32_t box_bytes = (uint32_t)boxr * RB * sizeof(c32);
-  auto column_of = [&](long long i) { return (int)blockIdx.x + (int)(i / pairs) * (int)gridDim.x; };
-  auto slice_of = [&](long long i, int b) { return NB * (int)(i % pairs) + b; };
-  auto issue = [&](long long i, int s) {
-    const int nb = min(NB, nslices - slice_of(i, 0));
-    mbar_expect_tx(&full[s], nb * nbox * box_bytes);
-    for (int b = 0; b < nb; ++b)
-      for (int q = 0; q < nbox; ++q)
-        tma_load_4d(inb + (s * NB + b) * CL + q * boxr * RB, &tmap, 0, column_of(i), q * boxr,
-                    slice_of(i, b), &full[s]);
-  };
-  if (t == 0) {
-    tma_prefetch_desc(&tmap);
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], TT);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (t == 0)
-    for (int s = 0; s < S && s < nitems; ++s) issue(s, s);
-
-  PassTw<M, E, FftShape<M, E>::NP - 1> last_tw;
-  if constexpr (CACHE) last_tw.from_table(t);
-  const TwLastCached<M, E> twc{&last_tw};
-  const TwDirect twt;
-  c32 pq[E];
-  float bi[FLIP ? E : 1];
-  const int col_len = nrb * RB;
-  for (long long i = 0; i < nitems; ++i) {
-    const int s = (int)(i % S);
-    const uint32_t parity = (uint32_t)((i / S) & 1);
-    if (i % pairs == 0) {
-      const long long c = column_of(i);
-#pragma unroll
-      for (int m = 0; m < E; ++m) {
-        pq[m] = __ldg(PQ + c * M + t + TT * m);
-        if constexpr (FLIP) bi[m] = __ldg(Bi + c * M + t + TT * m);
-      }
-    }
-    const int nb = min(NB, nslices - slice_of(i, 0));
-    mbar_wait(&full[s], parity);
-    c32 v[NB][E];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const c32* in = inb + (s * NB + b) * CL;
-#pragma unroll
-      for (int m = 0; m < E / 2; ++m) {
-        const int j = t + TT * m;
-        v[b][m] = (b < nb && j < col_len) ? in[j] : mk(0.f, 0.f);
-      }
-    }
-    mbar_arrive(&empty[s]);
-    if constexpr (CACHE) fftn<M, E, false, true, false, NB, TwLastCached<M, E>, PP>(v, xbuf, SB, t, twc);
-    else fftn<M, E, false, true, false, NB, TwDirect, PP>(v, xbuf, SB, t, twt);
-    // refill stage s with item i + S once every thread has released it
-    if (t == 0 && i + S < nitems) {
-      mbar_wait(&empty[s], parity);
-      issue(i + S, s);
-    }
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        if constexpr (FLIP) {
-          v[b][m] = pfma(mk(v[b][m].y, v[b][m].x), mk(bi[m], bi[m]), pmul(v[b][m], pq[m]));
-        } else {
-          v[b][m] = pmul(v[b][m], pq[m]);
-        }
-      }
-    if constexpr (CACHE) fftn<M, E, true, false, true, NB, TwLastCached<M, E>, PP>(v, xbuf, SB, t, twc);
-    else fftn<M, E, true, false, true, NB, TwDirect, PP>(v, xbuf, SB, t, twt);
-    if constexpr (PP) {
-      const int H = M / 2 + 1;
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        if (b >= nb) break;
-#pragma unroll
-        for (int m = 0; m < E / 2; ++m) {
-          const int j = t + TT * m;
-          if (j < col_len) T[tidx(slice_of(i, b), j, column_of(i), nrb, H)] = v[b][m];
-        }
-      }
-      continue;
-    }
-    // the previous item's TMA store must have finished reading the out buffer
-    if (t == 0) bulk_wait_read<0>();
-    __syncthreads();
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-#pragma unroll
-      for (int m = 0; m < E / 2; ++m) {
-        const int j = t + TT * m;
-        if (j < col_len) outb[b * CL + j] = v[b][m];
-      }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (t == 0) {
-      for (int b = 0; b < nb; ++b)
-        for (int q = 0; q < nbox; ++q)
-          tma_store_4d(&tmap, 0, column_of(i), q * boxr, slice_of(i, b),
-                       outb + b * CL + q * boxr * RB);
-      bulk_commit();
-    }
-  }
-  if (t == 0) bulk_wait<0>();
-}
-
-// twiddle source of the ping-pong column kernel (tuning: TF_K2_TWDIRECT=0 -> product tree)
-#ifndef TF_K2_TWDIRECT
-#define TF_K2_TWDIRECT 0
-#endif
-#if TF_K2_TWDIRECT == 1
-using K2Tw = TwDirect;
-#elif TF_K2_TWDIRECT == 2
-using K2Tw = TwMixed;
-#else
+// twiddles of the column kernel: table entry + product tree (table-loaded powers
+// measured slower: the last-pass table lives in L2)
 using K2Tw = TwTable;
-#endif
 
-// K2, ping-pong variant: same contract as k_cols_conv_tma<..., NB = 1>.
+// K2 for 1024 <= M <= 4096: a persistent, TMA-fed column kernel.  Each CTA walks
+// its (column, slice) items, column-major, keeping the column's PSF in registers
+// across all slices.  Thread 0 keeps the next S items in flight: TMA 4-D tensor
+// copies (box = 32 B x BOXR row blocks) gather the column's pieces from every
+// row block into a contiguous shared stage, completing on the stage's `full`
+// mbarrier; a stage is refilled only after every thread has arrived on its
+// `empty` mbarrier (release/acquire ordering of the generic reads before the
+// async-proxy write; a bare __syncthreads is not enough since BAR.SYNC lets the
+// issuing warp run ahead).
 // * the FFT exchanges alternate between two shared buffers, so each exchange
 //   costs one CTA barrier instead of two;
 // * results go straight to global memory: 8-byte stores, 4 consecutive lanes
@@ -833,11 +677,6 @@ constexpr int rows_g() {  // thread groups per CTA in K1/K3 (each group: NB row 
   constexpr int g = (NB == 2 ? 256 : 512) / T;
   return g < 1 ? 1 : (g > 16 ? 16 : g);
 }
-// row pairs per group in K1/K3: tuning knob TF_ROWS_NB (1 or 2; default 2)
-inline int rows_nb() {
-  static const int nb = getenv("TF_ROWS_NB") ? atoi(getenv("TF_ROWS_NB")) : 2;
-  return nb == 1 ? 1 : 2;
-}
 template <int M>
 constexpr int cols_g() {  // columns per CTA in the generic K2
   constexpr int T = M / eper<M>();
@@ -887,31 +726,22 @@ int launch_rows_fwd_pf(const float* x, c32* T, int rows, int n_in, long long xs,
   return check_launch("k_rows_fwd_pf");
 }
 
-// input prefetch variant: TF_ROWS_PF (default 1) when rows are 16-byte aligned blocks
-inline bool rows_pf() {
-  static const int pf = getenv("TF_ROWS_PF") ? atoi(getenv("TF_ROWS_PF")) : 1;
-  return pf != 0;
-}
 
 template <int M>
 int launch_rows_fwd(const float* x, c32* T, int rows, int n_in, long long xs, long long xr,
                     long long nslices, cudaStream_t st) {
   const size_t pf_smem = sizeof(c32) * 2 * group_stride(M, 2) + sizeof(float) * RB * n_in + 16;
-  if (M >= 1024 && rows_pf() && n_in % 4 == 0 && xr % 4 == 0 && xs % 4 == 0 &&
+  // persistent bulk-prefetched variant when rows are 16-byte aligned blocks
+  if (M >= 1024 && n_in % 4 == 0 && xr % 4 == 0 && xs % 4 == 0 &&
       reinterpret_cast<uintptr_t>(x) % 16 == 0 && pf_smem <= 200 * 1024)
     return launch_rows_fwd_pf<M>(x, T, rows, n_in, xs, xr, nslices, st);
-  if (M >= 1024 && rows_nb() == 1)
-    return launch_rows_fwd_t<M, 1>(x, T, rows, n_in, xs, xr, nslices, st);
   return launch_rows_fwd_t<M, 2>(x, T, rows, n_in, xs, xr, nslices, st);
 }
 
 // How many blocks ahead a K3 CTA prefetches the spectrum block and aux rows into
-// L2 (TF_K3_L2PF, default one per SM: about half a resident wave ahead; 0 = off).
-// Measured on 64 x 2048^2: 0.92 -> 0.78 ms (110-200 equal, 592 thrashes).
-inline int k3_l2pf() {
-  static const int v = getenv("TF_K3_L2PF") ? atoi(getenv("TF_K3_L2PF")) : num_sms();
-  return v;
-}
+// L2: one per SM, about half a resident wave ahead.  Measured on 64 x 2048^2:
+// 0.92 -> 0.78 ms (110-200 equal, 592 thrashes).
+inline int k3_l2pf() { return num_sms(); }
 
 template <int M, int NB>
 int launch_rows_inv_t(const c32* T, float* out, const float* aux, int rows, int n_out,
@@ -945,8 +775,6 @@ template <int M>
 int launch_rows_inv(const c32* T, float* out, const float* aux, int rows, int n_out,
                     long long os, long long orow, float alpha, float beta, long long nslices,
                     cudaStream_t st) {
-  if (M >= 1024 && rows_nb() == 1)
-    return launch_rows_inv_t<M, 1>(T, out, aux, rows, n_out, os, orow, alpha, beta, nslices, st);
   return launch_rows_inv_t<M, 2>(T, out, aux, rows, n_out, os, orow, alpha, beta, nslices, st);
 }
 
@@ -981,32 +809,6 @@ int encode_tmap(CUtensorMap* map, c32* T, int M, int nrb, long long nslices, int
 }
 
 constexpr int CONV_STAGES = 2;
-
-template <int M, bool FLIP, int NB, bool CACHE, bool PP = false, int EOVR = 0>
-int launch_cols_conv_tma_t(c32* T, const c32* PQ, const float* Bi, int col_len,
-                           long long nslices, cudaStream_t st) {
-  constexpr int E = EOVR ? EOVR : eper<M>();
-  constexpr int TT = M / E;
-  const int ncols = M / 2 + 1;
-  const int nrb = nrb_of(col_len);
-  const int boxr = std::min(nrb, 256);
-  CUtensorMap map;
-  TF_TRY(encode_tmap(&map, T, M, nrb, nslices, boxr));
-  const size_t smem = sizeof(c32) * ((size_t)((PP ? 0 : 1) + CONV_STAGES) * NB * (M / 2) +
-                                     (PP ? 2 : 1) * NB * group_stride(M, NB)) +
-                      2 * CONV_STAGES * sizeof(uint64_t);
-  auto kern = k_cols_conv_tma<M, E, CONV_STAGES, FLIP, NB, CACHE, PP>;
-  TF_TRY(prep_kernel(kern, smem));
-  int blocks_per_sm = 0;
-  TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, TT, smem),
-                    "occupancy"));
-  const int grid = std::max(1, std::min(ncols, std::max(1, blocks_per_sm) * num_sms()));
-  KernelTimer tm;
-  timer_begin(tm, 1, st);
-  kern<<<grid, TT, smem, st>>>(map, PQ, Bi, ncols, nrb, (int)nslices, boxr, T);
-  timer_end(tm);
-  return check_launch("k_cols_conv_tma");
-}
 
 template <int M, bool FLIP, int NS = CONV_STAGES>
 int launch_cols_conv_pp_t(c32* T, const c32* PQ, const float* Bi, int col_len,
@@ -1057,31 +859,9 @@ template <int M>
 int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
                      bool flip, cudaStream_t st) {
   if (2 * col_len > M) return fail_arg("k_cols_conv: column length %d exceeds M/2", col_len);
-  // tuning/debug knob: TF_K2 = pp (default) | nb1 | nb1c | nb2 | nb2c | nb1p | e8 | generic
-  static const char* k2 = getenv("TF_K2");
-  static const int variant = !k2 ? 6 : !strcmp(k2, "generic") ? -1 : !strcmp(k2, "nb1") ? 0
-                          : !strcmp(k2, "nb1c") ? 1 : !strcmp(k2, "nb2") ? 2 : !strcmp(k2, "nb1p") ? 4
-                          : !strcmp(k2, "e8") ? 5 : !strcmp(k2, "pp") ? 6 : !strcmp(k2, "pp1") ? 7 : 3;
   if constexpr (M >= 1024 && M <= 4096) {
-    switch (variant) {
-      case 0: return flip ? launch_cols_conv_tma_t<M, true, 1, false>(T, PQ, Bi, col_len, nslices, st)
-                          : launch_cols_conv_tma_t<M, false, 1, false>(T, PQ, Bi, col_len, nslices, st);
-      case 1: return flip ? launch_cols_conv_tma_t<M, true, 1, true>(T, PQ, Bi, col_len, nslices, st)
-                          : launch_cols_conv_tma_t<M, false, 1, true>(T, PQ, Bi, col_len, nslices, st);
-      case 2: return flip ? launch_cols_conv_tma_t<M, true, 2, false>(T, PQ, Bi, col_len, nslices, st)
-                          : launch_cols_conv_tma_t<M, false, 2, false>(T, PQ, Bi, col_len, nslices, st);
-      case 3: return flip ? launch_cols_conv_tma_t<M, true, 2, true>(T, PQ, Bi, col_len, nslices, st)
-                          : launch_cols_conv_tma_t<M, false, 2, true>(T, PQ, Bi, col_len, nslices, st);
-      case 4: return flip ? launch_cols_conv_tma_t<M, true, 1, false, true>(T, PQ, Bi, col_len, nslices, st)
-                          : launch_cols_conv_tma_t<M, false, 1, false, true>(T, PQ, Bi, col_len, nslices, st);
-      case 5: return flip ? launch_cols_conv_tma_t<M, true, 1, false, false, 8>(T, PQ, Bi, col_len, nslices, st)
-                          : launch_cols_conv_tma_t<M, false, 1, false, false, 8>(T, PQ, Bi, col_len, nslices, st);
-      case 6: return flip ? launch_cols_conv_pp_t<M, true>(T, PQ, Bi, col_len, nslices, st)
-                          : launch_cols_conv_pp_t<M, false>(T, PQ, Bi, col_len, nslices, st);
-      case 7: return flip ? launch_cols_conv_pp_t<M, true, 1>(T, PQ, Bi, col_len, nslices, st)
-                          : launch_cols_conv_pp_t<M, false, 1>(T, PQ, Bi, col_len, nslices, st);
-      default: break;
-    }
+    return flip ? launch_cols_conv_pp_t<M, true>(T, PQ, Bi, col_len, nslices, st)
+                : launch_cols_conv_pp_t<M, false>(T, PQ, Bi, col_len, nslices, st);
   }
   return flip ? launch_cols_conv_t<M, true>(T, PQ, Bi, col_len, nslices, st)
               : launch_cols_conv_t<M, false>(T, PQ, Bi, col_len, nslices, st);

@@ -15,7 +15,6 @@ from __future__ import annotations
 import collections
 import functools
 import math
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -40,8 +39,6 @@ __all__ = [
 
 # slices processed per apply pass; bounds the half-spectrum workspace
 _MAX_CHUNK_BYTES = 4 << 30
-# slices per K1 -> K2 -> K3 pass (0: as many as the workspace allows); tuning knob
-_CHUNK_SLICES = int(os.environ.get("TF_CHUNK_SLICES", "0"))
 
 
 def _is_7smooth(v: int) -> bool:
@@ -219,7 +216,7 @@ def apply_stack(psf: PsfKernel, x: torch.Tensor, out: torch.Tensor | None = None
     if aux is not None and (aux.shape != x.shape or not aux.is_contiguous()):
         raise ValueError("aux must match the input stack")
     per_slice = lib.tf_toeplitz_workspace_bytes(n, m, 1)
-    chunk = max(1, min(z, _MAX_CHUNK_BYTES // per_slice, _CHUNK_SLICES or z))
+    chunk = max(1, min(z, _MAX_CHUNK_BYTES // per_slice))
     ws = _device.workspace(per_slice * chunk)
     _lib.check(
         lib.tf_toeplitz_apply(x.data_ptr(), out.data_ptr(), _lib.ptr(aux), float(alpha),

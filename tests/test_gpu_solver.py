@@ -283,7 +283,7 @@ def test_early_stop_records_and_snapshots(tf):
     assert not last.restarted and abs(last.objective - recs[-2].objective) <= tol * abs(
         recs[-2].objective)
     assert [k for k, _ in snaps] == list(range(1, k_stop + 1))
-    np.testing.assert_array_equal(snaps[-1][1], rec)
+    np.testing.assert_array_equal(snaps[-1][1].reshape(np.shape(rec)), rec)  # (1, n, n) as the reference
     fixed, frecs = tf.solve(ctx, prm, tf.SolverConfig(max_iters=k_stop, tol=1e-300,
                                                       lipschitz=float(d["L"])), d["f0"][0])
     np.testing.assert_array_equal(fixed, rec)
