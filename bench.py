@@ -184,6 +184,65 @@ def cpu_sample(threads: int | None = None, slices: int | None = None, repeats: i
     return psf, x, rs, threads, slices, times
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_mbir_sample(psf, threads: int, slab: int = 2):
+    """BASELINE.md §3 legs (ii)/(iii): the reference loop's per-iteration work
+    (solver.py:147-178: two _apply_batch, prior_grad, prior_energy -- the oracle
+    restatement, numpy) on 2048^2 slabs of ``slab`` slices, on 1 thread and on
+    ``threads`` threads at once (one slab per thread, as distributed_solve's slab
+    workers, runtime.py:622-691), plus the C4 extrapolation (labelled)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle as O
+
+    pr = O.Prior(sigma=0.1, lam=5e-4)
+    rng = np.random.default_rng(9)
+    vols = [rng.standard_normal((slab, N_SIDE, N_SIDE)) for _ in range(threads)]
+
+    def one_iter(v):
+        ky = O.apply_batch(psf, v)
+        g = ky + pr.lam * O.prior_grad(pr, v)
+        fn = v - 1e-6 * g
+        O.apply_batch(psf, fn)
+        O.prior_energy(pr, fn)
+
+    t0 = time.perf_counter()
+    one_iter(vols[0])
+    t1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one_iter, vols))
+    tw = time.perf_counter() - t0
+    per_slice_1 = t1 / slab
+    per_slice_w = tw / (slab * threads)
+    # C4 extrapolation: per-slice cost scaled by side^2 log2 side per level
+    cost = lambda side: per_slice_w * (side / N_SIDE) ** 2 * np.log2(2 * side) / np.log2(2 * N_SIDE)  # noqa: E731
+    c4_iter = N_SIDE * cost(N_SIDE)
+    c4_sched = sum(side * it * cost(side) for side, it in ((512, 40), (1024, 20), (2048, 10)))
+    return {
+        "unit": "s per slice-iteration at 2048^2",
+        "single_thread": per_slice_1, "threads": threads, "all_threads": per_slice_w,
+        "thread_speedup": per_slice_1 / per_slice_w,
+        "sample": f"one iteration of the reference loop's work (2 x _apply_batch, prior_grad, "
+                  f"prior_energy; oracle restatement) on a {slab} x 2048^2 slab, 1 thread, then "
+                  f"{threads} slabs on {threads} threads",
+        "c4_extrapolated_s_per_finest_iteration": c4_iter,
+        "c4_extrapolated_schedule_s": c4_sched,
+        "extrapolation": "EXTRAPOLATED, not measured: all_threads per-slice cost x slices, "
+                         "scaled by side^2 log2(2 side) per level; C4 schedule (512, 1024, 2048) "
+                         "x (40, 20, 10) iterations, setup excluded",
+    }
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -207,6 +266,7 @@ def run_reference(args, world, rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
                          "sample": f"{threads} slices of 2048^2 per step, one per host thread "
                                    "(numpy restatement of toeplitz._apply_batch: complex128 fft2 "
                                    "on the odd 4375^2 padded grid)"},
@@ -307,10 +367,12 @@ def run_ours(args, world, rank, local):
         mbir = _mbir(tf, args, world, rank)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        _, _, _, threads, slices, times = cpu_sample()
+        psf_o, _, _, threads, slices, times = cpu_sample()
         cpu = {"value": slices / min(times), "unit": UNIT, "cores": threads, "kind": "port",
+               "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
                "sample": f"{slices} slices of 2048^2, one per host thread, oracle port of "
-                         "toeplitz._apply_batch (complex128 fft2 on the odd 4375^2 grid) minus R*g"}
+                         "toeplitz._apply_batch (complex128 fft2 on the odd 4375^2 grid) minus R*g",
+               "mbir": cpu_mbir_sample(psf_o, threads)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -571,9 +633,27 @@ def _c4(args, world, rank):
     peak_gb = torch.cuda.max_memory_allocated() / 1e9
     t0 = time.perf_counter()
     out = np.empty(tuple(est.shape), dtype=np.float32)
-    step = 64
-    for z0 in range(0, est.shape[0], step):
-        out[z0:z0 + step] = est[z0:z0 + step].cpu().numpy()
+    step = 32
+    stages = [torch.empty((step,) + tuple(est.shape[1:]), dtype=torch.float32, pin_memory=True)
+              for _ in range(2)]
+    evs = [None, None]
+    pend = [None, None]
+    for i, z0 in enumerate(range(0, est.shape[0], step)):
+        b = i % 2
+        if evs[b] is not None:
+            evs[b].synchronize()
+            lo, hi = pend[b]
+            out[lo:hi] = stages[b][:hi - lo].numpy()
+        z1 = min(est.shape[0], z0 + step)
+        stages[b][:z1 - z0].copy_(est[z0:z1], non_blocking=True)
+        evs[b] = torch.cuda.Event()
+        evs[b].record()
+        pend[b] = (z0, z1)
+    for b in sorted(range(2), key=lambda q: pend[q][0] if pend[q] else -1):
+        if pend[b] is not None:
+            evs[b].synchronize()
+            lo, hi = pend[b]
+            out[lo:hi] = stages[b][:hi - lo].numpy()
     t_d2h = max_over_ranks(time.perf_counter() - t0, world)
     finite = bool(np.isfinite(out[::97]).all())
     del out, est

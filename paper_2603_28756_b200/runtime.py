@@ -225,6 +225,37 @@ class SlabComm:
         full = torch.cat([bufs[p.worker_id][:p.size] for p in parts])
         return full.to(slab.device)
 
+    def gather_range(self, slab: torch.Tensor, parts, ranges):
+        """Planes [lo, hi) = ``ranges[self.rank]`` of the volume distributed as ``parts``,
+        by point-to-point transfers of only the overlapping planes (every rank knows
+        every rank's range).  Replaces a whole-volume all-gather at a level change:
+        a fine slab's Lanczos z-taps need its own coarse planes +-3."""
+        me = parts[self.rank]
+        lo, hi = ranges[self.rank]
+        staged = not (self.direct and slab.is_cuda)
+        dev = torch.device("cpu") if staged else slab.device
+        out = torch.empty((hi - lo,) + tuple(slab.shape[1:]), dtype=slab.dtype, device=dev)
+        src = slab.to(dev) if staged else slab
+        ops = []
+        for q, (qlo, qhi) in enumerate(ranges):  # what I send to q
+            a, b = max(me.begin, qlo), min(me.end, qhi)
+            if a >= b:
+                continue
+            if q == self.rank:
+                out[a - lo:b - lo] = src[a - me.begin:b - me.begin]
+            else:
+                ops.append(dist.P2POp(dist.isend, src[a - me.begin:b - me.begin].contiguous(),
+                                      self._peer(q), self.group))
+        for q, p in enumerate(parts):  # what I receive from q
+            a, b = max(p.begin, lo), min(p.end, hi)
+            if a >= b or q == self.rank:
+                continue
+            ops.append(dist.P2POp(dist.irecv, out[a - lo:b - lo], self._peer(q), self.group))
+        for req in (dist.batch_isend_irecv(ops) if ops else []):
+            req.wait()
+        self.counts["range"] += 1
+        return out.to(slab.device)
+
     def gather(self, slab: torch.Tensor, parts, root: int = 0):
         """Full volume on ``root`` (None elsewhere); slabs padded to the largest size."""
         big = max(p.size for p in parts)
@@ -237,6 +268,35 @@ class SlabComm:
         if self.rank != root:
             return None
         return torch.cat([bufs[p.worker_id][:p.size] for p in parts])
+
+
+class _Rows:
+    """The sinogram a slab solve reads from: a ``Sinogram``, or the path of a saved
+    one (fileio format), memory-mapped so that each rank touches only its own rows
+    (a 2048^3 scan is 4.3 GB of float64 per process otherwise)."""
+
+    def __init__(self, sino):
+        if isinstance(sino, Sinogram):
+            self.angles, self._data = sino.angles, sino.data
+            return
+        from . import fileio
+
+        path = __import__("pathlib").Path(sino)
+        head = fileio._read_header(path)
+        if head["kind"] != "sinogram":
+            raise ValueError(f"{path} holds a {head['kind']}, not a sinogram")
+        self.angles = np.asarray(head["angles"], dtype=np.float64)
+        self._data = np.memmap(path, dtype="<f8", mode="r", shape=tuple(head["dims"]))
+
+    slices = property(lambda self: self._data.shape[0])
+    detector_bins = property(lambda self: self._data.shape[2])
+
+    def rows(self, idx) -> np.ndarray:
+        """float64 rows of slices ``idx`` (a slice or index array): only those are read."""
+        return np.asarray(self._data[idx], dtype=np.float64)
+
+    def sinogram(self) -> Sinogram:
+        return Sinogram(angles=self.angles, data=self.rows(slice(None)))
 
 
 def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig, n_workers: int,
@@ -252,11 +312,13 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
     own slab as a device tensor.  ``on_record`` / ``snapshot_sink`` fire on rank
     0 only (snapshots gather the full volume every iteration -- tests only).
     ``transport`` is accepted for signature compatibility; the transport is the
-    process group.
+    process group.  ``sino`` may also be the path of a saved sinogram: each rank
+    then reads only its own rows (memory-mapped).
     """
+    src = _Rows(sino)
     if n_workers < 1:
         raise ValueError("need at least one worker")
-    if n_workers > sino.slices:
+    if n_workers > src.slices:
         raise ValueError("more workers than slices")
     if gather not in ("root", "none"):
         raise ValueError("gather must be 'root' or 'none'")
@@ -264,20 +326,20 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
     if n_workers != world and not (n_workers == 1 and world == 1):
         raise ValueError(f"n_workers={n_workers} must equal the process-group size {world} "
                          "(one process per GPU; launch with torchrun)")
-    geom = ScanGeometry(angles=sino.angles, detector_bins=sino.detector_bins,
+    geom = ScanGeometry(angles=src.angles, detector_bins=src.detector_bins,
                         image_side=image_side)
     sampling = polar_sampling(geom)
     plan = NufftPlan(image_side, sampling, nufft_tolerance, oversampling)
     psf = build_psf(sampling, image_side, nufft_tolerance, oversampling)
-    if f0 is not None and (f0.slices != sino.slices or f0.side != image_side):
+    if f0 is not None and (f0.slices != src.slices or f0.side != image_side):
         raise ValueError("initial volume does not match the requested reconstruction")
 
     if n_workers == 1:
         L = cfg.lipschitz if cfg.lipschitz is not None else estimate_lipschitz(psf, params)
         cfg1 = SolverConfig(max_iters=cfg.max_iters, tol=cfg.tol, lipschitz=L,
                             restart=cfg.restart, log_every=cfg.log_every, nonneg=cfg.nonneg)
-        ctx = fidelity_context(plan, psf, sino)
-        x0 = f0 if f0 is not None else torch.zeros((sino.slices, image_side, image_side),
+        ctx = fidelity_context(plan, psf, sino if isinstance(sino, Sinogram) else src.sinogram())
+        x0 = f0 if f0 is not None else torch.zeros((src.slices, image_side, image_side),
                                                    device=_lib.device())
         vol, records = solve(ctx, params, cfg1, x0, on_record=on_record,
                              snapshot_sink=snapshot_sink)
@@ -288,14 +350,14 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
         return vol, records
 
     rank = dist.get_rank(group)
-    parts = partition(sino.slices, n_workers)
+    parts = partition(src.slices, n_workers)
     part = parts[rank]
     comm = SlabComm(part, group)
     try:
         L = cfg.lipschitz
         if L is None:
             L = comm.broadcast_scalar(estimate_lipschitz(psf, params) if rank == 0 else None)
-        rows = sino.data[part.begin:part.end]
+        rows = src.rows(slice(part.begin, part.end))
         ctx = FidelityContext(psf=psf, rstar=back_project_stack(plan, rows),
                               g_norm_sq=float(np.sum(rows ** 2)))
         if f0 is None:
@@ -303,7 +365,7 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
         else:
             x0 = torch.from_numpy(np.ascontiguousarray(f0.data[part.begin:part.end],
                                                        dtype=np.float32)).to(_lib.device())
-        stencil = stencil_3d() if sino.slices > 1 else stencil_2d()
+        stencil = stencil_3d() if src.slices > 1 else stencil_2d()
         sink = None
         if snapshot_sink is not None:
             def sink(k, slab):
@@ -340,31 +402,33 @@ def distributed_solve_hierarchical(full_sino: Sinogram, hierarchy, params, cfg: 
     see exactly the single-GPU inputs.  Returns ``(volume, per-level records)``
     as ``solve_hierarchical`` (volume on rank 0 with ``gather="root"``).
     """
-    from .multires import _strided_indices, upsample_slab
+    from .multires import _strided_indices, slab_source_range, upsample_slab
     from .radon import fbp_stack
 
+    src = _Rows(full_sino)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if n_workers != world:
         raise ValueError(f"n_workers={n_workers} must equal the process-group size {world}")
     if world == 1:
         from .multires import solve_hierarchical
 
-        return solve_hierarchical(full_sino, hierarchy, params, cfg, use_fbp_init=use_fbp_init,
+        full = full_sino if isinstance(full_sino, Sinogram) else src.sinogram()
+        return solve_hierarchical(full, hierarchy, params, cfg, use_fbp_init=use_fbp_init,
                                   downsample_angles=downsample_angles,
                                   nufft_tolerance=nufft_tolerance, oversampling=oversampling,
                                   on_record=on_record)
     target = hierarchy.levels[-1]
-    if full_sino.detector_bins < target:
+    if src.detector_bins < target:
         raise ValueError("detector does not cover the target grid")
     rank = dist.get_rank(group)
     n_levels = len(hierarchy.levels)
     all_records, estimate, parts_prev = [], None, None
     for lvl, side in enumerate(hierarchy.levels):
         factor = 1 << (n_levels - 1 - lvl)
-        bins = _strided_indices(full_sino.detector_bins, factor) if factor > 1 else None
-        zidx = (_strided_indices(full_sino.slices, factor)
-                if factor > 1 and full_sino.slices > 1 else np.arange(full_sino.slices))
-        angles = full_sino.angles
+        bins = _strided_indices(src.detector_bins, factor) if factor > 1 else None
+        zidx = (_strided_indices(src.slices, factor)
+                if factor > 1 and src.slices > 1 else np.arange(src.slices))
+        angles = src.angles
         keep = np.arange(0, angles.size, factor) if (downsample_angles and factor > 1) else None
         if keep is not None:
             angles = angles[keep]
@@ -373,7 +437,7 @@ def distributed_solve_hierarchical(full_sino: Sinogram, hierarchy, params, cfg: 
             raise ValueError(f"level {lvl} has {n_z} slices for {n_workers} workers")
         parts = partition(n_z, n_workers)
         part = parts[rank]
-        rows = full_sino.data[zidx[part.begin:part.end]]
+        rows = src.rows(zidx[part.begin:part.end])  # this rank's rows only
         if bins is not None:
             rows = rows[:, :, bins] / factor
         if keep is not None:
@@ -393,8 +457,12 @@ def distributed_solve_hierarchical(full_sino: Sinogram, hierarchy, params, cfg: 
             x0 = (fbp_stack(plan, rows) if use_fbp_init else
                   torch.zeros((part.size, side, side), device=_lib.device()))
         else:
-            coarse = SlabComm(parts_prev[rank], group).allgather(estimate, parts_prev)
-            x0 = upsample_slab(coarse, side, n_z, part.begin, part.end)
+            # only the coarse planes each fine slab's z-taps reach travel (p2p)
+            ranges = [slab_source_range(parts_prev[-1].end, n_z, p.begin, p.end) for p in parts]
+            coarse = SlabComm(parts_prev[rank], group).gather_range(estimate, parts_prev, ranges)
+            estimate = None
+            x0 = upsample_slab(coarse, side, n_z, part.begin, part.end, src_begin=ranges[rank][0],
+                               n_src=parts_prev[-1].end)
         cfg_l = SolverConfig(max_iters=hierarchy.iters_per_level[lvl], tol=cfg.tol, lipschitz=L,
                              restart=cfg.restart, log_every=cfg.log_every, nonneg=cfg.nonneg)
         sink = ((lambda rec, _l=lvl: on_record(_l, rec))

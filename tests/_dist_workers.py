@@ -27,8 +27,13 @@ def comm_worker(rank, world, port, n_slices, side, out_dir):
         lo, hi = comm.exchange(slab)
         red = comm.allreduce(torch.tensor([1.0, float(rank), float(part.size)], dtype=torch.float64))
         g = comm.gather(slab, parts)
+        # level-change transfer: rank r needs planes [r, n_slices - world + r + 1) (overlapping
+        # ranges of different lengths, crossing several slabs)
+        ranges = [(q, n_slices - world + q + 1) for q in range(world)]
+        rng_planes = comm.gather_range(slab, parts, ranges)
         res = {"lo": None if lo is None else lo.numpy(), "hi": None if hi is None else hi.numpy(),
-               "red": red.numpy(), "halo_msgs": comm.counts["halo"]}
+               "red": red.numpy(), "halo_msgs": comm.counts["halo"],
+               "range": rng_planes.numpy(), "range_lohi": ranges[rank]}
         if rank == 0:
             res["gather"] = g.numpy()
         np.save(os.path.join(out_dir, f"rank{rank}.npy"), res, allow_pickle=True)
@@ -51,10 +56,18 @@ def solve_worker(rank, world, port, fixture, out_dir):
         snaps = []
         vol, recs = distributed_solve(sino, 16, prm, cfg, world,
                                       snapshot_sink=lambda k, v: snaps.append(v))
+        # the same solve from a saved sinogram: each rank memory-maps its own rows
+        from paper_2603_28756_b200 import fileio
+
+        path = os.path.join(out_dir, "sino.raw")
+        if rank == 0:
+            fileio.save_array(path, sino)
+        dist.barrier()
+        vol_p, _ = distributed_solve(path, 16, prm, cfg, world)
         if rank == 0:
             np.save(os.path.join(out_dir, "solve.npy"),
                     {"vol": vol.data, "obj": np.array([r.objective for r in recs]),
-                     "nsnap": len(snaps)}, allow_pickle=True)
+                     "nsnap": len(snaps), "vol_path": vol_p.data}, allow_pickle=True)
     finally:
         dist.destroy_process_group()
 

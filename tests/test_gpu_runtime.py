@@ -49,6 +49,7 @@ def test_two_workers_match_single_worker(tf, tmp_path):
     assert rel_l2(r["vol"], d["recon_w2"]) < 1e-3
     np.testing.assert_allclose(r["obj"], d["obj_w2"], rtol=1e-4)
     assert r["nsnap"] == 8
+    np.testing.assert_array_equal(r["vol_path"], r["vol"])  # sinogram read per rank from a file
 
 
 def test_worker_count_must_match_group(tf):

@@ -73,6 +73,8 @@ def test_slab_comm_gloo(tmp_path, world, n_slices):
             else:
                 np.testing.assert_array_equal(got, want)
         np.testing.assert_array_equal(r["red"], [world, sum(range(world)), n_slices])
+        lo_, hi_ = r["range_lohi"]
+        np.testing.assert_array_equal(r["range"], full[lo_:hi_])  # p2p level-change planes
         assert r["halo_msgs"] == (p.lower is not None) + (p.upper is not None)
     r0 = np.load(tmp_path / "rank0.npy", allow_pickle=True).item()
     np.testing.assert_array_equal(r0["gather"], full)
