@@ -459,9 +459,13 @@ def _mbir(tf, args, world, rank):
     peak = _peak_hbm()["value"]
     del ctx, f0
     torch.cuda.empty_cache()
+    slab = _slab_iteration(tf, world, rank, timed)
+    torch.cuda.empty_cache()
     if world > 1:
-        return _mbir_distributed(tf, z, world, rank, prm, L, timed, {
+        out = _mbir_distributed(tf, z, world, rank, prm, L, timed, {
             "psf": t_psf, "rstar_nufft": t_rstar, "fbp_nufft": t_fbp}, per_it, bpv, peak)
+        out["slab256_iteration"] = slab
+        return out
     hier = tf.GridHierarchy(levels=(512, 1024, 2048), iters_per_level=(40, 20, 10))
     run_hier = lambda: tf.solve_hierarchical(  # noqa: E731
         sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300, lipschitz=L), use_fbp_init=True)
@@ -484,6 +488,7 @@ def _mbir(tf, args, world, rank):
     c1 = None if args.no_cpu_baseline else _c1_pipeline(tf, timed)
     return {
         "workload": f"C3 slab: {z} x 2048^2 per GPU, 128 angles, Nd=2048, qGGMRF lam=5e-4",
+        "slab256_iteration": slab,
         "c1_end_to_end": c1,
         "setup_ms": {"psf": t_psf, "rstar_nufft": t_rstar, "fbp_nufft": t_fbp},
         "solve_ms_per_iter": per_it,
@@ -543,20 +548,11 @@ def _c1_pipeline(tf, timed):
 def _mbir_distributed(tf, z, world, rank, prm, L, timed, setup, per_it_local, bpv, peak):
     """N > 1: the z-slab solver over NCCL (runtime.distributed_solve, one slab of
     ``z`` slices per rank, halo exchange + 3-scalar allreduce every iteration)."""
-    from paper_2603_28756_b200.runtime import distributed_solve
-
-    g = np.random.default_rng(4100).standard_normal((z * world, N_ANGLES, N_BINS))
-    sino = tf.Sinogram(angles=angles(), data=g)
-    iters = 10
-    cfg = tf.SolverConfig(max_iters=iters, tol=1e-300, lipschitz=L)
-    distributed_solve(sino, N_SIDE, prm, tf.SolverConfig(max_iters=2, tol=1e-300, lipschitz=L),
-                      world, gather="none")  # warm (plans, PSF, NCCL channels)
-    (_, recs), t_total = timed(lambda: distributed_solve(sino, N_SIDE, prm, cfg, world,
-                                                         gather="none"))
-    step_ms = max_over_ranks(float(np.median([r.step_time for r in recs[1:]])) * 1e3, world)
     from paper_2603_28756_b200.runtime import distributed_solve_hierarchical
 
     hier = tf.GridHierarchy(levels=(512, 1024, 2048), iters_per_level=(40, 20, 10))
+    g = np.random.default_rng(4100).standard_normal((z * world, N_ANGLES, N_BINS))
+    sino = tf.Sinogram(angles=angles(), data=g)
     _, t_hier = timed(lambda: distributed_solve_hierarchical(
         sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300, lipschitz=L), world,
         use_fbp_init=True, gather="none"))
@@ -565,14 +561,37 @@ def _mbir_distributed(tf, z, world, rank, prm, L, timed, setup, per_it_local, bp
                     "128 angles, Nd=2048, qGGMRF lam=5e-4",
         "setup_ms_per_gpu": setup,
         "solve_ms_per_iter_single_gpu_slab": per_it_local,
-        "distributed_ms_per_iter": step_ms,
-        "distributed_total_ms_incl_setup": t_total,
         "hierarchical_3level_ms": t_hier,
         "hierarchical_schedule": "levels (512, 1024, 2048), iterations (40, 20, 10), FBP init, "
-                                 "re-partitioned z-slabs per level, Lanczos-3 upsampling",
-        "solve_bytes_per_voxel_iter": bpv,
-        "solve_hbm_frac": bpv * z * N_SIDE * N_SIDE / (step_ms / 1e3) / 1e9 / peak,
+                                 "re-partitioned z-slabs per level (p2p coarse planes), Lanczos-3",
         "comm_per_iter": "2 halo planes of 16.8 MB per interior boundary + one 3 x fp64 allreduce",
+    }
+
+
+def _slab_iteration(tf, world, rank, timed, slices=256, iters=10):
+    """The full MBIR iteration (K4 + Toeplitz apply + K5 + decision, plus the NCCL halo
+    exchange and scalar allreduce for N > 1) on a fixed C4 slab of ``slices`` x 2048^2
+    PER GPU (runtime.distributed_solve; N = 1 is the single-GPU solve): weak scaling of
+    the iteration that C4 runs 10 times at its finest level."""
+    from paper_2603_28756_b200.runtime import distributed_solve
+
+    g = np.random.default_rng(4200).standard_normal((slices * world, N_ANGLES, N_BINS))
+    sino = tf.Sinogram(angles=angles(), data=g)
+    prm = tf.QggmrfParams(sigma=0.5, lam=5e-4)
+    cfg = tf.SolverConfig(max_iters=iters, tol=1e-300, lipschitz=2.0e6)
+    distributed_solve(sino, N_SIDE, prm, tf.SolverConfig(max_iters=2, tol=1e-300, lipschitz=2.0e6),
+                      world, gather="none")  # warm (plans, PSF, NCCL channels)
+    (_, recs), t_total = timed(lambda: distributed_solve(sino, N_SIDE, prm, cfg, world,
+                                                         gather="none"))
+    step_ms = max_over_ranks(float(np.median([r.step_time for r in recs[2:]])) * 1e3, world)
+    peak = _peak_hbm()["value"]
+    return {
+        "workload": f"{slices} x 2048^2 per GPU ({slices * world} slices on {world} GPU(s)), "
+                    "128 angles, Nd=2048, qGGMRF lam=5e-4, fixed L",
+        "ms_per_iter": step_ms,
+        "slices_per_s": slices * world / (step_ms / 1e3),
+        "hbm_frac_at_88B": 88.0 * slices * N_SIDE * N_SIDE / (step_ms / 1e3) / 1e9 / peak,
+        "total_ms_incl_setup": t_total, "iters": iters, "scaling": "weak",
     }
 
 
