@@ -106,6 +106,37 @@ int tf_prior_update_dc(const float* d_f, const float* d_f_lo, const float* d_f_h
                        double T, const double* weights3, double* d_ws, double* d_gsq,
                        void* stream);
 
+/* tf_prior_update_dc (write_grad = 0, 3-D) run only when *d_only_if != 0 (the
+ * restart flag of tf_solver_decide's record), with c = *d_c: the solver re-runs
+ * the update after a restart; otherwise the launch (and the *d_gsq write) is a
+ * no-op.  The momentum argument is taken from d_c only. */
+int tf_prior_update_if(const float* d_f, const float* d_f_lo, const float* d_f_hi,
+                       const float* d_fp, const float* d_fp_lo, const float* d_fp_hi,
+                       const float* d_Kf, const float* d_Kfp, const float* d_rstar, float* d_out,
+                       int nz, int h, int w, const float* d_c, float lam, float inv_L, int nonneg,
+                       double sigma, double p, double q, double T, const double* weights3,
+                       double* d_ws, double* d_gsq, const double* d_only_if, void* stream);
+
+/* K45: one pass over a 3-D slab that computes tf_energy_fid's sums for the
+ * current iterate f (= d_f, previous iterate d_fp, K f = d_Kf, K f_prev = d_Kfp)
+ *   *d_energy = E(f) (half stencil + pairs into d_f_hi; 0 if !with_prior),
+ *   *d_fid = <f, K f / 2 - R*g>,  *d_dfid = <f - f_prev, (K f + K f_prev)/2 - R*g>
+ * together with tf_prior_update_dc's update for the NEXT iterate,
+ *   d_out = y - (K y - R*g + lam grad_prior(y)) inv_L,  y = f + c (f - f_prev),
+ * with c the no-restart momentum (t - 1) / t', t' = (1 + sqrt(1 + 4 t^2)) / 2,
+ * t = d_state[3], in tf_solver_decide's fp64 arithmetic; *d_gsq = sum grad^2.
+ * (solver.py:147-180 / qggmrf.py:172-217.)  If the decision for f restarts, the
+ * caller re-runs the update with tf_prior_update_if.  d_out may alias d_Kfp;
+ * output pointers may be NULL (not written). */
+int tf_prior_energy_update(const float* d_f, const float* d_f_lo, const float* d_f_hi,
+                           const float* d_fp, const float* d_fp_lo, const float* d_fp_hi,
+                           const float* d_Kf, const float* d_Kfp, const float* d_rstar,
+                           float* d_out, int nz, int h, int w, const double* d_state, float lam,
+                           float inv_L, int nonneg, int with_prior, double sigma, double p,
+                           double q, double T, const double* weights3, double* d_ws,
+                           double* d_energy, double* d_fid, double* d_dfid, double* d_gsq,
+                           void* stream);
+
 /* The restart / momentum / stop decision of one iteration, on the device
  * (tomoforge/solver.py:147-180: restart when the objective increases, momentum
  * t' = (1 + sqrt(1 + 4 t^2)) / 2, stop when |dobj| <= tol |obj| without a restart).

@@ -50,6 +50,14 @@ _SIGNATURES = {
                                                        _c_float, _c_float, _c_int, _c_int, _c_int,
                                                        _c_double, _c_double, _c_double, _c_double,
                                                        _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
+    "tf_prior_update_if": (_c_int, [_c_void_p] * 10 + [_c_int, _c_int, _c_int, _c_void_p, _c_float,
+                                                       _c_float, _c_int, _c_double, _c_double,
+                                                       _c_double, _c_double, _c_void_p, _c_void_p,
+                                                       _c_void_p, _c_void_p, _c_void_p]),
+    "tf_prior_energy_update": (_c_int, [_c_void_p] * 10 + [_c_int, _c_int, _c_int, _c_void_p,
+                                                           _c_float, _c_float, _c_int, _c_int,
+                                                           _c_double, _c_double, _c_double,
+                                                           _c_double] + [_c_void_p] * 7),
     "tf_solver_decide": (_c_int, [_c_void_p] * 4 + [_c_double, _c_int, _c_int, _c_double,
                                                     _c_void_p]),
     "tf_energy_fid": (_c_int, [_c_void_p] * 6 + [_c_int, _c_int, _c_int, _c_int, _c_int, _c_double,

@@ -109,7 +109,13 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
                  const float* rstar, float* f_new, int nz, int h, int w_, float c, float lam,
                  float inv_L, int nonneg, int write_grad, int three_d, double sigma, double p,
                  double q, double T, const double* w, double* partial, double* out_gsq,
-                 const float* c_dev, cudaStream_t st);
+                 const float* c_dev, cudaStream_t st, const double* only_if);
+int prior_energy_update(const float* f, const float* f_lo, const float* f_hi, const float* fp,
+                        const float* fp_lo, const float* fp_hi, const float* Kf, const float* Kfp,
+                        const float* rstar, float* f_new, int nz, int h, int w_, const double* state,
+                        float lam, float inv_L, int nonneg, int with_prior, double sigma, double p,
+                        double q, double T, const double* w, double* partial, double* out_e,
+                        double* out_fid, double* out_dfid, double* out_gsq, cudaStream_t st);
 int solver_decide(const double* vals, double* state, float* c_out, double* rec, double lam,
                   int with_prior, int restart, double tol, cudaStream_t st);
 int energy_fid(const float* fn, const float* fn_hi, const float* f, const float* Kfn,
@@ -257,7 +263,47 @@ int tf_prior_update_dc(const float* d_f, const float* d_f_lo, const float* d_f_h
     return fail_arg("halo planes of f and f_prev must both be given");
   return prior_update(d_f, d_f_lo, d_f_hi, d_fp, d_fp_lo, d_fp_hi, d_Kf, d_Kfp, d_rstar, d_out, nz,
                       h, w, c, lam, inv_L, nonneg, write_grad, three_d, sigma, p, q, T, weights3, d_ws,
-                      d_gsq, d_c, (cudaStream_t)stream);
+                      d_gsq, d_c, (cudaStream_t)stream, nullptr);
+}
+
+int tf_prior_update_if(const float* d_f, const float* d_f_lo, const float* d_f_hi,
+                       const float* d_fp, const float* d_fp_lo, const float* d_fp_hi,
+                       const float* d_Kf, const float* d_Kfp, const float* d_rstar, float* d_out,
+                       int nz, int h, int w, const float* d_c, float lam, float inv_L, int nonneg,
+                       double sigma, double p, double q, double T, const double* weights3,
+                       double* d_ws, double* d_gsq, const double* d_only_if, void* stream) {
+  TF_TRY(ensure_init());
+  TF_TRY(check_prior(h, w, nz, sigma, p, q, T));
+  if (!d_f || !d_fp || !d_out || !d_ws || !d_gsq || !weights3 || !d_c || !d_only_if)
+    return fail_arg("null pointer");
+  if ((d_Kf == nullptr) != (d_Kfp == nullptr)) return fail_arg("Kf and Kfp must both be given");
+  if ((d_f_lo == nullptr) != (d_fp_lo == nullptr) || (d_f_hi == nullptr) != (d_fp_hi == nullptr))
+    return fail_arg("halo planes of f and f_prev must both be given");
+  return prior_update(d_f, d_f_lo, d_f_hi, d_fp, d_fp_lo, d_fp_hi, d_Kf, d_Kfp, d_rstar, d_out, nz,
+                      h, w, 0.f, lam, inv_L, nonneg, 0, 1, sigma, p, q, T, weights3, d_ws, d_gsq, d_c,
+                      (cudaStream_t)stream, d_only_if);
+}
+
+int tf_prior_energy_update(const float* d_f, const float* d_f_lo, const float* d_f_hi,
+                           const float* d_fp, const float* d_fp_lo, const float* d_fp_hi,
+                           const float* d_Kf, const float* d_Kfp, const float* d_rstar,
+                           float* d_out, int nz, int h, int w, const double* d_state, float lam,
+                           float inv_L, int nonneg, int with_prior, double sigma, double p,
+                           double q, double T, const double* weights3, double* d_ws,
+                           double* d_energy, double* d_fid, double* d_dfid, double* d_gsq,
+                           void* stream) {
+  TF_TRY(ensure_init());
+  TF_TRY(check_prior(h, w, nz, sigma, p, q, T));
+  if (!d_f || !d_fp || !d_Kf || !d_Kfp || !d_rstar || !d_out || !d_ws || !weights3 || !d_state)
+    return fail_arg("null pointer");
+  if ((d_f_lo == nullptr) != (d_fp_lo == nullptr) || (d_f_hi == nullptr) != (d_fp_hi == nullptr))
+    return fail_arg("halo planes of f and f_prev must both be given");
+  if (d_out == d_f || d_out == d_fp || d_out == d_Kf || d_out == d_rstar)
+    return fail_arg("output may alias only d_Kfp");
+  return prior_energy_update(d_f, d_f_lo, d_f_hi, d_fp, d_fp_lo, d_fp_hi, d_Kf, d_Kfp, d_rstar,
+                             d_out, nz, h, w, d_state, lam, inv_L, nonneg, with_prior, sigma, p, q,
+                             T, weights3, d_ws, d_energy, d_fid, d_dfid, d_gsq,
+                             (cudaStream_t)stream);
 }
 
 int tf_solver_decide(const double* d_vals, double* d_state, float* d_c, double* d_rec, double lam,

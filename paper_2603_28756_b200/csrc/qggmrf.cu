@@ -400,7 +400,13 @@ struct SymTile {
   }
 };
 
-template <int RY, bool P2, bool NONNEG, bool EDGE>
+// FUSED (K45): additionally the K5 sums of the CURRENT iterate F -- its energy
+// over the half stencil (+ pairs into F.hi), <F, Kf/2 - R*g> and the increment
+// <F - FP, (Kf + Kfp)/2 - R*g> -- from the same tiles and operands, while the
+// update part computes the NEXT iterate at y = F + c (F - FP) with the momentum
+// c of the no-restart branch.  F's planes are staged in fsf; partial[4 b + j] =
+// {E(F), fid, dfid, sum grad^2}.
+template <int RY, bool P2, bool NONNEG, bool EDGE, bool FUSED = false>
 __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP,
                                                const float* __restrict__ Kf,
                                                const float* Kfp,  // may alias f_new
@@ -408,8 +414,12 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
                                                float* f_new, double* partial, int nz,
                                                int h, int w, float c, float lam, float inv_L,
                                                int write_grad, const PriorConsts& pc, float* ysf,
-                                               float* gsf, double* red) {
+                                               float* gsf, double* red, float* fsf = nullptr,
+                                               bool energy = false) {
   using S = SymTile<RY>;
+  // per-voxel operands: Kf, Kfp, R*g (+ FP when fused)
+  constexpr int NOP = FUSED ? 4 : 3;
+  using Ops = float[NOP][RY];
   constexpr int CELLS = S::CELLS, NT = S::NT;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int gx0 = blockIdx.y * S::H, gy0 = blockIdx.x * S::W;
@@ -462,7 +472,7 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
       hp[m] = v ? __ldg(pp + coff[m]) : 0.f;
     }
   };
-  auto fetch_ops = [&](int zz, float (&o)[3][RY]) {
+  auto fetch_ops = [&](int zz, Ops& o) {
     if (zz >= nz) return;
     const long long base = zz * nn;
 #pragma unroll
@@ -472,25 +482,34 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
         o[1][r] = inside[r] ? Kfp[base + vo[r]] : 0.f;  // may alias f_new
       }
       if (rstar) o[2][r] = inside[r] ? __ldg(rstar + base + vo[r]) : 0.f;
+      if constexpr (FUSED) o[NOP - 1][r] = inside[r] ? __ldg(FP.main + base + vo[r]) : 0.f;
     }
   };
 
   const float glam = lam * pc.inv_sp;
   const bool has_lo = FP.lo != nullptr;
-  double gsq = 0.0;
-  float opA[3][RY], opB[3][RY];
+  double gsq = 0.0, e_acc = 0.0, fid = 0.0, dfid = 0.0;
+  Ops opA, opB;
 #pragma unroll
-  for (int r = 0; r < RY; ++r) opA[0][r] = opA[1][r] = opA[2][r] = opB[0][r] = opB[1][r] = opB[2][r] = 0.f;
+  for (int j = 0; j < NOP; ++j)
+#pragma unroll
+    for (int r = 0; r < RY; ++r) opA[j][r] = opB[j][r] = 0.f;
 
   // One plane step; S0 = z & 1 is a compile-time constant, so every shared-memory
   // offset below is an immediate.  `cur` holds this plane's operands, `nxt`
   // receives the next plane's.
-  auto step = [&](auto s0c, int z, float (&cur)[3][RY], float (&nxt)[3][RY]) {
+  auto step = [&](auto s0c, int z, Ops& cur, Ops& nxt) {
     constexpr int S0 = decltype(s0c)::value, S1 = S0 ^ 1;
     float* yw = ysf + S1 * CELLS + threadIdx.x;  // plane z+1 lands in slot S1
 #pragma unroll
     for (int m = 0; m < S::SLOTS; ++m)
       if (m + 1 < S::SLOTS || last_ok) yw[m * NT] = fmaf(c, hf[m] - hp[m], hf[m]);
+    if constexpr (FUSED) {
+      float* fw = fsf + S1 * CELLS + threadIdx.x;
+#pragma unroll
+      for (int m = 0; m < S::SLOTS; ++m)
+        if (m + 1 < S::SLOTS || last_ok) fw[m * NT] = hf[m];
+    }
     fetch_plane(z + 2);
     fetch_ops(z + 1, nxt);
     __syncthreads();
@@ -563,6 +582,52 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
       }
     }
     (void)strip_d;
+    // ---- fused: energy of F's plane z over the half stencil (K5's sums)
+    float xf[RY];
+    (void)xf;
+    if constexpr (FUSED) {
+      const float* fa = fsf + S0 * CELLS;
+      const float* fb = fsf + S1 * CELLS;
+      const float up = (z + 1 < nz || F.hi != nullptr) ? 1.f : 0.f;
+      float eacc[RY];
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        xf[r] = fa[me0 + r * TY * S::RW];
+        eacc[r] = 0.f;
+      }
+      if (energy && z >= 0) {
+        constexpr int NE = 13 * RY, NEV = (NE + 1) & ~1;
+        float2 x2 = mk(0.f, 0.f), n2 = mk(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < NEV; ++e) {
+          float xs = 0.f, xn = 0.f;
+          if (e < NE) {
+            const int r = e / 13, k = e % 13;
+            xs = xf[r];
+            xn = (k < 4 ? fa : fb)[me0 + r * TY * S::RW + S::off(k)];
+          }
+          if (e & 1) {
+            x2.y = xs;
+            n2.y = xn;
+            const float2 g = rho2<P2>(csub(x2, n2), pc);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int ee = e - 1 + h2;
+              if (ee < NE) {
+                const int r = ee / 13, k = ee % 13;
+                eacc[r] = fmaf(k < 4 ? wgt(r, k, 1) : wgt(r, k, 1) * up, h2 ? g.y : g.x, eacc[r]);
+              }
+            }
+          } else {
+            x2.x = xs;
+            n2.x = xn;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+          if (inside[r]) e_acc += (double)(eacc[r] * pc.inv_psp);
+      }
+    }
     __syncthreads();
     // ---- phase B: backward terms, gradient, update
     if (z >= 0) {
@@ -584,6 +649,13 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
         const float prior = (f_in[r] - b_in) + ((hi_ok ? f_x[r] : 0.f) - b_x);
         const float ky = fmaf(c, cur[0][r] - cur[1][r], cur[0][r]);
         const float grad = fmaf(glam, prior, ky - cur[2][r]);
+        if constexpr (FUSED) {
+          if (inside[r]) {  // K5's fidelity sums of F (fp32 products, fp64 running sums)
+            const float fnv = xf[r], kfn = cur[0][r], kf = cur[1][r], rs = cur[2][r];
+            fid += (double)(fnv * fmaf(0.5f, kfn, -rs));
+            dfid += (double)((fnv - cur[NOP - 1][r]) * (fmaf(0.5f, kfn + kf, 0.f) - rs));
+          }
+        }
         if (inside[r]) {
           if (write_grad) {
             outz[vo[r]] = grad;
@@ -607,6 +679,12 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
 #pragma unroll
     for (int m = 0; m < S::SLOTS; ++m)
       if (m + 1 < S::SLOTS || last_ok) yw[m * NT] = fmaf(c, hf[m] - hp[m], hf[m]);
+    if constexpr (FUSED) {
+      float* fw = fsf + (z0 & 1) * CELLS + threadIdx.x;
+#pragma unroll
+      for (int m = 0; m < S::SLOTS; ++m)
+        if (m + 1 < S::SLOTS || last_ok) fw[m * NT] = hf[m];
+    }
   }
   fetch_plane(z0 + 1);
   if (has_lo) step(I1{}, -1, opB, opA);  // cliques halo -> plane 0; fetches plane 0's operands
@@ -615,8 +693,22 @@ __device__ __forceinline__ void prior_sym_tile(const Planes& F, const Planes& FP
     step(I0{}, z, opA, opB);
     if (z + 1 < nz) step(I1{}, z + 1, opB, opA);
   }
-  const double r = block_sum_d<NT>(gsq, red);
-  if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = r;
+  const int b = blockIdx.y * gridDim.x + blockIdx.x;
+  if constexpr (FUSED) {
+    const double r0 = block_sum_d<NT>(e_acc, red);
+    const double r1 = block_sum_d<NT>(fid, red);
+    const double r2 = block_sum_d<NT>(dfid, red);
+    const double r3 = block_sum_d<NT>(gsq, red);
+    if (threadIdx.x == 0) {
+      partial[4 * b] = r0;
+      partial[4 * b + 1] = r1;
+      partial[4 * b + 2] = r2;
+      partial[4 * b + 3] = r3;
+    }
+  } else {
+    const double r = block_sum_d<NT>(gsq, red);
+    if (threadIdx.x == 0) partial[b] = r;
+  }
 }
 
 #ifndef TF_K4_RY
@@ -632,9 +724,11 @@ __global__ void __launch_bounds__(TX* TY, TF_K4_MINB)
 k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const float* Kfp,
                    const float* __restrict__ rstar, float* f_new,
                    double* __restrict__ partial, int nz, int h, int w, float c, float lam,
-                   float inv_L, int write_grad, PriorConsts pc, const float* __restrict__ c_dev) {
+                   float inv_L, int write_grad, PriorConsts pc, const float* __restrict__ c_dev,
+                   const double* __restrict__ only_if) {
   using S = SymTile<K4_RY>;
   extern __shared__ float sym_smem[];
+  if (only_if && *only_if == 0.0) return;  // conditional re-run (after a restart only)
   if (c_dev) c = *c_dev;  // momentum decided on the device (tf_solver_decide)
   __shared__ double red[TX * TY / 32];
   float* ys = sym_smem;                // [2][CELLS]
@@ -649,9 +743,42 @@ k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const floa
                                             lam, inv_L, write_grad, pc, ys, gs, red);
 }
 
-static size_t sym_smem_bytes() {
+// K45: K5 of iteration k fused with K4 of iteration k+1 (one pass over the slab
+// instead of two; same transcendental work).  The momentum of the no-restart
+// branch is computed here from the device state with tf_solver_decide's exact
+// fp64 arithmetic, so when iteration k does not restart the result is the one
+// the unfused K5 -> decide -> K4 sequence gives; after a restart the solver
+// re-runs K4 with c = 0 (k_prior_update_sym with `only_if` = the restart flag).
+template <bool P2, bool NONNEG>
+__global__ void __launch_bounds__(TX* TY, 2)
+k_prior_energy_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* Kfp,
+                      const float* __restrict__ rstar, float* f_new, double* __restrict__ partial,
+                      int nz, int h, int w, float lam, float inv_L, int energy, PriorConsts pc,
+                      const double* __restrict__ state) {
   using S = SymTile<K4_RY>;
-  return sizeof(float) * (2 + S::GSLOTS) * S::CELLS;
+  extern __shared__ float sym_smem[];
+  __shared__ double red[TX * TY / 32];
+  const double t = state[3];
+  const double t_next = __dadd_rn(1.0, sqrt(__dadd_rn(1.0, __dmul_rn(__dmul_rn(4.0, t), t)))) / 2.0;
+  const float c = (float)((t - 1.0) / t_next);
+  float* ys = sym_smem;                                   // [2][CELLS]
+  float* gs = sym_smem + 2 * S::CELLS;                    // [GSLOTS][CELLS]
+  float* fs = sym_smem + (2 + S::GSLOTS) * S::CELLS;      // [2][CELLS]
+  const bool interior = blockIdx.y * S::H >= 1 && (blockIdx.y + 1) * S::H + 1 <= h &&
+                        blockIdx.x * S::W >= 1 && (blockIdx.x + 1) * S::W + 1 <= w;
+  if (interior)
+    prior_sym_tile<K4_RY, P2, NONNEG, false, true>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w,
+                                                   c, lam, inv_L, 0, pc, ys, gs, red, fs,
+                                                   energy != 0);
+  else
+    prior_sym_tile<K4_RY, P2, NONNEG, true, true>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w,
+                                                  c, lam, inv_L, 0, pc, ys, gs, red, fs,
+                                                  energy != 0);
+}
+
+static size_t sym_smem_bytes(bool fused = false) {
+  using S = SymTile<K4_RY>;
+  return sizeof(float) * (2 + S::GSLOTS + (fused ? 2 : 0)) * S::CELLS;
 }
 static dim3 sym_grid(int h, int w) {
   using S = SymTile<K4_RY>;
@@ -781,6 +908,22 @@ k_sum_partials(const double* __restrict__ partial, int nblocks, int nv, double* 
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x) s += partial[(long long)b * nv + j];
     const double r = block_sum_d<1024>(s, red);
     if (threadIdx.x == 0) out[j] = r;
+  }
+}
+
+// out_j = sum_b partial[b*nv + j] for the non-null out_j (j < 4); skipped entirely
+// when only_if points at 0.0 (the conditional K4 after a restart decision)
+__global__ void __launch_bounds__(1024)
+k_sum_partials_to(const double* __restrict__ partial, int nblocks, int nv, double* o0,
+                  double* o1, double* o2, double* o3, const double* __restrict__ only_if) {
+  if (only_if && *only_if == 0.0) return;
+  __shared__ double red[32];
+  double* outs[4] = {o0, o1, o2, o3};
+  for (int j = 0; j < nv; ++j) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) s += partial[(long long)b * nv + j];
+    const double r = block_sum_d<1024>(s, red);
+    if (threadIdx.x == 0 && outs[j]) *outs[j] = r;
   }
 }
 
@@ -1026,7 +1169,8 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
                  const float* rstar, float* f_new, int nz, int h, int w_, float c, float lam, float inv_L,
                  int nonneg, int write_grad, int three_d, double sigma, double p, double q,
                  double T, const double* w, double* partial, double* out_gsq, const float* c_dev,
-                 cudaStream_t st) {
+                 cudaStream_t st, const double* only_if) {
+  if (only_if && !three_d) return fail_arg("conditional update is 3-D only");
   const PriorConsts pc = make_consts(sigma, p, q, T, w);
   const dim3 grid = tile_grid(h, w_);
   const Planes F{f, f_lo, f_hi}, FP{fp, fp_lo, fp_hi};
@@ -1040,7 +1184,8 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
   do {                                                                                       \
     TF_TRY(prep_kernel(k_prior_update_sym<P2V, NN>, ssmem));                                 \
     k_prior_update_sym<P2V, NN><<<sgrid, TX * TY, ssmem, st>>>(                              \
-        F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, c, lam, inv_L, write_grad, pc, c_dev); \
+        F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, c, lam, inv_L, write_grad, pc, c_dev, \
+        only_if);                                                                            \
   } while (0)
   // 3-D: the symmetric-clique tile kernel; 2-D (single slices): the direct stencil
   if (three_d) {
@@ -1054,7 +1199,33 @@ int prior_update(const float* f, const float* f_lo, const float* f_hi, const flo
 #undef TF_K4S
   TF_TRY(check_launch("k_prior_update"));
   const int nparts = three_d ? (int)(sgrid.x * sgrid.y) : (int)(grid.x * grid.y);
-  k_sum_partials<<<1, 1024, 0, st>>>(partial, nparts, 1, out_gsq);
+  k_sum_partials_to<<<1, 1024, 0, st>>>(partial, nparts, 1, out_gsq, nullptr, nullptr, nullptr,
+                                        only_if);
+  return check_launch("k_sum_partials");
+}
+
+int prior_energy_update(const float* f, const float* f_lo, const float* f_hi, const float* fp,
+                        const float* fp_lo, const float* fp_hi, const float* Kf, const float* Kfp,
+                        const float* rstar, float* f_new, int nz, int h, int w_, const double* state,
+                        float lam, float inv_L, int nonneg, int with_prior, double sigma, double p,
+                        double q, double T, const double* w, double* partial, double* out_e,
+                        double* out_fid, double* out_dfid, double* out_gsq, cudaStream_t st) {
+  const PriorConsts pc = make_consts(sigma, p, q, T, w);
+  const Planes F{f, f_lo, f_hi}, FP{fp, fp_lo, fp_hi};
+  const dim3 sgrid = sym_grid(h, w_);
+  const size_t smem = sym_smem_bytes(true);
+#define TF_K45(P2V, NN)                                                                      \
+  do {                                                                                       \
+    TF_TRY(prep_kernel(k_prior_energy_update<P2V, NN>, smem));                               \
+    k_prior_energy_update<P2V, NN><<<sgrid, TX * TY, smem, st>>>(                            \
+        F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, lam, inv_L, with_prior, pc, state); \
+  } while (0)
+  if (p == 2.0) { if (nonneg) TF_K45(true, true); else TF_K45(true, false); }
+  else { if (nonneg) TF_K45(false, true); else TF_K45(false, false); }
+#undef TF_K45
+  TF_TRY(check_launch("k_prior_energy_update"));
+  k_sum_partials_to<<<1, 1024, 0, st>>>(partial, (int)(sgrid.x * sgrid.y), 4, out_e, out_fid,
+                                        out_dfid, out_gsq, nullptr);
   return check_launch("k_sum_partials");
 }
 

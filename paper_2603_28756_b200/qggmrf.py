@@ -164,14 +164,15 @@ def _weights_ptr(stencil: NeighborStencil):
 
 def prior_update(params, stencil, f, fp, out, *, kf=None, kfp=None, rstar=None, c=0.0, lam=1.0,
                  inv_L=0.0, nonneg=False, write_grad=False, f_lo=None, f_hi=None, fp_lo=None,
-                 fp_hi=None, c_dev=None) -> torch.Tensor:
-    """K4 launch on device stacks; returns a device fp64 tensor [sum(grad^2)].
-    ``c_dev`` (fp32 device scalar) overrides ``c`` on the device (solver_decide)."""
+                 fp_hi=None, c_dev=None, gsq_out=None) -> torch.Tensor:
+    """K4 launch on device stacks; returns a device fp64 tensor [sum(grad^2)] (or
+    writes it to the fp64 device scalar ``gsq_out``).  ``c_dev`` (fp32 device
+    scalar) overrides ``c`` on the device (solver_decide)."""
     lib = _lib.ensure_ready()
     z, h, w_ = f.shape
     wsb = lib.tf_prior_workspace_bytes(h, w_)
     ws = _device.workspace(wsb, tag="prior")
-    gsq = torch.empty(1, dtype=torch.float64, device=f.device)
+    gsq = torch.empty(1, dtype=torch.float64, device=f.device) if gsq_out is None else gsq_out
     w, wp = _weights_ptr(stencil)
     P = _lib.ptr
     _lib.check(lib.tf_prior_update_dc(
@@ -180,6 +181,41 @@ def prior_update(params, stencil, f, fp, out, *, kf=None, kfp=None, rstar=None, 
         int(stencil.three_d), *_consts(params), wp, ws.data_ptr(), gsq.data_ptr(),
         _lib.stream_handle()), "tf_prior_update_dc")
     return gsq
+
+
+def prior_update_if(params, stencil, f, out, *, kf, rstar, c_dev, only_if, gsq_out, lam, inv_L,
+                    nonneg=False, f_lo=None, f_hi=None):
+    """K4 at y = f (c = *c_dev, 0 after a restart) run only when *only_if != 0: the
+    re-run of the update after a restart decision (tf_prior_update_if).  Writes
+    sum grad^2 to the fp64 device scalar ``gsq_out`` (a tensor view)."""
+    lib = _lib.ensure_ready()
+    z, h, w_ = f.shape
+    ws = _device.workspace(lib.tf_prior_workspace_bytes(h, w_), tag="prior")
+    w, wp = _weights_ptr(stencil)
+    P = _lib.ptr
+    _lib.check(lib.tf_prior_update_if(
+        P(f), P(f_lo), P(f_hi), P(f), P(f_lo), P(f_hi), P(kf), P(kf), P(rstar), P(out), z, h, w_,
+        P(c_dev), float(lam), float(inv_L), int(bool(nonneg)), *_consts(params), wp,
+        ws.data_ptr(), gsq_out.data_ptr(), only_if.data_ptr(), _lib.stream_handle()),
+        "tf_prior_update_if")
+
+
+def prior_energy_update(params, stencil, f, fp, out, *, kf, kfp, rstar, state, lam, inv_L,
+                        nonneg=False, with_prior=True, f_lo=None, f_hi=None, fp_lo=None,
+                        fp_hi=None, energy=None, fid=None, dfid=None, gsq=None):
+    """K45 (tf_prior_energy_update): K5's sums for f and the no-restart update of
+    the next iterate in one pass; the sums land in the given fp64 device scalars
+    (tensor views, or None)."""
+    lib = _lib.ensure_ready()
+    z, h, w_ = f.shape
+    ws = _device.workspace(lib.tf_prior_workspace_bytes(h, w_), tag="prior")
+    w, wp = _weights_ptr(stencil)
+    P = _lib.ptr
+    _lib.check(lib.tf_prior_energy_update(
+        P(f), P(f_lo), P(f_hi), P(fp), P(fp_lo), P(fp_hi), P(kf), P(kfp), P(rstar), P(out), z, h,
+        w_, P(state), float(lam), float(inv_L), int(bool(nonneg)), int(bool(with_prior)),
+        *_consts(params), wp, ws.data_ptr(), P(energy), P(fid), P(dfid), P(gsq),
+        _lib.stream_handle()), "tf_prior_energy_update")
 
 
 def solver_decide(vals, state, c_dev, rec, *, lam, with_prior, restart, tol):

@@ -320,3 +320,62 @@ def test_cuda_input_is_not_modified(tf):
     assert torch.equal(f0, keep)
     host, _ = tf.solve(ctx, prm, cfg, d["f0"])
     np.testing.assert_array_equal(out.cpu().numpy().astype(np.float64), host)
+
+
+@pytest.mark.parametrize("shape,halos", [((5, 72, 100), False), ((4, 49, 161), True),
+                                         ((1, 33, 40), True)])
+def test_fused_energy_update_matches_k5_k4(tf, rng, shape, halos):
+    """K45 (tf_prior_energy_update) = K5's sums of f + K4's update at the no-restart
+    momentum, bit for bit; the conditional re-run (tf_prior_update_if) is a no-op
+    unless the restart flag is set, and then equals K4 at c = 0."""
+    import math
+
+    import torch
+
+    from paper_2603_28756_b200.qggmrf import (energy_fid, prior_energy_update, prior_update,
+                                              prior_update_if)
+
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()  # noqa: E731
+    prm = tf.QggmrfParams(sigma=0.3, lam=0.7, p=2.0, q=1.2, T=1.0)
+    s3 = tf.stencil_3d()
+    f, fp = dev(rng.standard_normal(shape)), dev(rng.standard_normal(shape))
+    kf, kfp, rs = (dev(rng.standard_normal(shape)) for _ in range(3))
+    pl = lambda: dev(rng.standard_normal(shape[1:])) if halos else None  # noqa: E731
+    f_lo, f_hi, fp_lo, fp_hi = pl(), pl(), pl(), pl()
+    if not halos:
+        f_lo = f_hi = fp_lo = fp_hi = None
+    t = 2.37
+    state = torch.tensor([0.0, 0.0, 0.0, t, 0.0], dtype=torch.float64, device="cuda")
+    t_next = (1.0 + math.sqrt(1.0 + 4.0 * t * t)) / 2.0
+    c = float(np.float32((t - 1.0) / t_next))
+    lam, inv_L = 0.7, 0.05
+    ref_out = torch.empty_like(f)
+    gsq_ref = prior_update(prm, s3, f, fp, ref_out, kf=kf, kfp=kfp, rstar=rs, c=c, lam=lam,
+                           inv_L=inv_L, f_lo=f_lo, f_hi=f_hi, fp_lo=fp_lo, fp_hi=fp_hi)
+    e3 = energy_fid(prm, s3, f, fn_hi=f_hi, f=fp, kfn=kf, kf=kfp, rstar=rs)
+    out = kfp.clone()  # the solver writes over K f_prev
+    kfp_in = kfp.clone()
+    sums = torch.zeros(4, dtype=torch.float64, device="cuda")
+    prior_energy_update(prm, s3, f, fp, out, kf=kf, kfp=out, rstar=rs, state=state, lam=lam,
+                        inv_L=inv_L, f_lo=f_lo, f_hi=f_hi, fp_lo=fp_lo, fp_hi=fp_hi,
+                        energy=sums[0], fid=sums[1], dfid=sums[2], gsq=sums[3])
+    assert torch.equal(out, ref_out)
+    got = sums.cpu().numpy()
+    ref = e3.cpu().numpy()
+    np.testing.assert_allclose(got[:3], ref, rtol=1e-12)
+    assert got[3] == float(gsq_ref)
+    assert torch.equal(kfp, kfp_in)
+    # conditional re-run: flag 0 -> untouched; flag 1 -> K4 at y = f with c = *c_dev = 0
+    flag = torch.zeros(1, dtype=torch.float64, device="cuda")
+    c0 = torch.zeros(1, dtype=torch.float32, device="cuda")
+    g2 = torch.full((1,), -1.0, dtype=torch.float64, device="cuda")
+    prior_update_if(prm, s3, f, out, kf=kf, rstar=rs, c_dev=c0, only_if=flag[0], gsq_out=g2[0],
+                    lam=lam, inv_L=inv_L, f_lo=f_lo, f_hi=f_hi)
+    assert torch.equal(out, ref_out) and float(g2) == -1.0
+    flag.fill_(1.0)
+    prior_update_if(prm, s3, f, out, kf=kf, rstar=rs, c_dev=c0, only_if=flag[0], gsq_out=g2[0],
+                    lam=lam, inv_L=inv_L, f_lo=f_lo, f_hi=f_hi)
+    ref0 = torch.empty_like(f)
+    gsq0 = prior_update(prm, s3, f, f, ref0, kf=kf, kfp=kf, rstar=rs, c=0.0, lam=lam,
+                        inv_L=inv_L, f_lo=f_lo, f_hi=f_hi, fp_lo=f_lo, fp_hi=f_hi)
+    assert torch.equal(out, ref0) and float(g2) == float(gsq0)
