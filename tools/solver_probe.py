@@ -9,7 +9,8 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_28756_b200 as tf  # noqa: E402
-from paper_2603_28756_b200.qggmrf import energy_fid, prior_update, stencil_3d  # noqa: E402
+from paper_2603_28756_b200.qggmrf import (energy_fid, prior_energy_update, prior_update,  # noqa: E402
+                                          stencil_3d)
 from paper_2603_28756_b200.toeplitz import FidelityContext  # noqa: E402
 
 z = int(os.environ.get("PROBE_SLICES", "64"))
@@ -42,6 +43,11 @@ res = {}
 res["k4_prior_update_ms"] = ev(lambda: prior_update(prm, st, f, fp, out, kf=kf, kfp=kfp, rstar=rs,
                                                     c=0.3, lam=5e-4, inv_L=1e-3))
 res["k5_energy_fid_ms"] = ev(lambda: energy_fid(prm, st, out, f=f, kfn=kf, kf=kfp, rstar=rs))
+state = torch.tensor([0.0, 0.0, 0.0, 2.0, 0.0], dtype=torch.float64, device=dev)
+sums = torch.zeros(4, dtype=torch.float64, device=dev)
+res["k45_energy_update_ms"] = ev(lambda: prior_energy_update(
+    prm, st, f, fp, out, kf=kf, kfp=kfp, rstar=rs, state=state, lam=5e-4, inv_L=1e-3,
+    energy=sums[0], fid=sums[1], dfid=sums[2], gsq=sums[3]))
 res["k5_fid_only_ms"] = ev(lambda: energy_fid(prm, st, out, f=f, kfn=kf, kf=kfp, rstar=rs,
                                               with_prior=False))
 ctx = FidelityContext(psf=psf, rstar=rs, g_norm_sq=1.0)
