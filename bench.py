@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-mbir", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--c4-side", type=int, default=2048, help="C4 volume side (2048 = configs[3])")
+    ap.add_argument("--no-c5", action="store_true")
     return ap.parse_args()
 
 
@@ -297,6 +298,7 @@ def run_ours(args, world, rank, local):
     dev = torch.device("cuda", torch.cuda.current_device())
     # C4 first, on a clean device (R*g + 4 volumes of 2048^3 take ~175 of 191 GB)
     c4 = None if args.no_c4 else _c4(args, world, rank)
+    c5 = None if args.no_c5 else _c5(args, world, rank)
     z = args.slices
     geom = tf.ScanGeometry(angles=angles(), detector_bins=N_BINS, image_side=N_SIDE)
     psf = tf.build_psf(tf.polar_sampling(geom), N_SIDE)
@@ -381,6 +383,7 @@ def run_ours(args, world, rank, local):
             "data": "synthetic: randn volume, R*g from a randn sinogram",
             "config": config(args, world), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": launches, "mbir": mbir, "mbir_c4": c4,
+            "mbir_c5": c5,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -703,6 +706,75 @@ def _c4(args, world, rank):
         "synthesis_s_untimed": t_synth,
         "finite": finite,
     }
+
+
+def _c5(args, world, rank):
+    """configs[4] (C5): 2560^2 x 512 laminography-style volume, 120 angles uniform in a
+    [0, 2 pi / 3) wedge, Nd = 2560, noise rms 0.5; the 3-level (640, 1280, 2560)
+    schedule from FBP and from zero (the reference's bench_init comparison,
+    bench.py:108-131) -- fidelity per iteration for both inits.
+    N = 2560 runs on the power-of-two FFT grid M = 8192 (no radix-5 passes)."""
+    import torch
+
+    import paper_2603_28756_b200 as tf
+    from paper_2603_28756_b200.multires import solve_hierarchical_device
+    from paper_2603_28756_b200.phantoms import shepp_logan_slab
+    from paper_2603_28756_b200.radon import forward_project_stack
+
+    n, z, nd, n_ang = 2560, 512, 2560, 120
+    free, _ = torch.cuda.mem_get_info()
+    need = 5 * 4 * n * n * z / world + 12e9
+    if free < need:
+        return {"skipped": f"needs ~{need / 1e9:.0f} GB free per GPU, {free / 1e9:.0f} GB free"}
+    ang = np.linspace(0.0, 2.0 * np.pi / 3.0, n_ang, endpoint=False)
+    geom = tf.ScanGeometry(angles=ang, detector_bins=nd, image_side=n)
+    plan = tf.NufftPlan(n, tf.polar_sampling(geom), 1e-6)
+    rows = np.empty((z, n_ang, nd), dtype=np.float32)
+    gen = torch.Generator(device="cuda").manual_seed(55)
+    for z0 in range(0, z, 32):
+        z1 = min(z, z0 + 32)
+        r = forward_project_stack(plan, shepp_logan_slab(n, z, z0, z1))
+        r += 0.5 * torch.randn(r.shape, device=r.device, generator=gen)
+        rows[z0:z1] = r.cpu().numpy()
+    del r
+    sino = tf.Sinogram(angles=ang, data=rows)
+    del rows
+    tf.clear_caches()
+    torch.cuda.empty_cache()
+    hier = tf.GridHierarchy(levels=(640, 1280, 2560), iters_per_level=(20, 10, 10))
+    prm = tf.QggmrfParams(sigma=0.1, lam=5e-4)
+    out = {"config": f"C5: {n}^2 x {z} 3-D Shepp-Logan, {n_ang} angles in [0, 2pi/3), Nd={nd}, "
+                     f"noise rms 0.5, levels {hier.levels} x {hier.iters_per_level}, qGGMRF "
+                     "sigma=0.1 lam=5e-4, per-level power-iteration L; FFT grid 8192 at the "
+                     "finest level", "n_gpus": world}
+    for name, fbp_init in (("fbp", True), ("zero", False)):
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        if world == 1:
+            est, lrecs = solve_hierarchical_device(sino, hier, prm,
+                                                   tf.SolverConfig(max_iters=1, tol=1e-300),
+                                                   use_fbp_init=fbp_init)
+        else:
+            from paper_2603_28756_b200.runtime import distributed_solve_hierarchical
+
+            est, lrecs = distributed_solve_hierarchical(
+                sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300), world,
+                use_fbp_init=fbp_init, gather="none")
+        torch.cuda.synchronize()
+        t = max_over_ranks(time.perf_counter() - t0, world)
+        del est
+        torch.cuda.empty_cache()
+        out[name] = {
+            "end_to_end_s": t,
+            "fidelity_per_level": [[r.fidelity for r in recs] for recs in lrecs],
+            "restarts": [int(sum(r.restarted for r in recs)) for recs in lrecs],
+            "ms_per_iter_finest": 1e3 * float(np.median([r.step_time for r in lrecs[-1][2:]])),
+        }
+    f0, fz = out["fbp"]["fidelity_per_level"], out["zero"]["fidelity_per_level"]
+    out["fbp_over_zero_initial_fidelity"] = f0[0][0] / fz[0][0]
+    out["fbp_over_zero_final_fidelity"] = f0[-1][-1] / fz[-1][-1]
+    return out
 
 
 def _peak_hbm():

@@ -325,6 +325,43 @@ def c3_chain():
     print("c3_chain.npz written")
 
 
+def c5_wedge():
+    """C5 (configs[4]) geometry at reduced size: 4 x 320^2 3-D Shepp-Logan, 120 angles
+    uniform in [0, 2 pi / 3) (limited-angle wedge), Nd = 320, Gaussian noise rms 0.5
+    (seed 7), qGGMRF lam = 5e-4, sigma = 0.1 range(FBP), L by power iteration, 30
+    iterations from FBP and from zero -- the reference's bench_init comparison
+    (bench.py:108-131) on the wedge.  Float32-rounded sinogram, as c2_full."""
+    sys.path.insert(0, str(REF))
+    import tomoforge as tf
+    from tomoforge import solver
+
+    side, n_ang, bins, z = 320, 120, 320, 4
+    ang = np.linspace(0.0, 2.0 * np.pi / 3.0, n_ang, endpoint=False)
+    geom = tf.ScanGeometry(angles=ang, detector_bins=bins, image_side=side)
+    samp = tf.polar_sampling(geom)
+    plan = tf.NufftPlan(side, samp, 1e-6)
+    psf = tf.build_psf(samp, side, 1e-6)
+    truth = tf.shepp_logan(side, three_d=True, slices=z)
+    clean = tf.project_volume(plan, truth).data
+    g = (clean + 0.5 * np.random.default_rng(7).standard_normal(clean.shape)).astype(np.float32)
+    sino = tf.Sinogram(angles=ang, data=g.astype(np.float64))
+    ctx = tf.fidelity_context(plan, psf, sino)
+    f_fbp = tf.fbp(plan, sino)
+    sigma = 0.1 * float(f_fbp.data.max() - f_fbp.data.min())
+    prm = tf.QggmrfParams(sigma=sigma, lam=5e-4)
+    L = solver.estimate_lipschitz(psf, prm)
+    cfg = tf.SolverConfig(max_iters=30, tol=1e-300, lipschitz=L)
+    out = {"angles": ang, "g": g, "sigma": sigma, "L": L}
+    for name, f0 in (("fbp", f_fbp), ("zero", tf.Volume(np.zeros((z, side, side))))):
+        rec, recs = tf.solve(ctx, prm, cfg, f0)
+        out[f"recon_{name}"] = rec.data.astype(np.float32)
+        out[f"fidelity_{name}"] = np.array([r.fidelity for r in recs])
+        out[f"objective_{name}"] = np.array([r.objective for r in recs])
+        out[f"restarted_{name}"] = np.array([r.restarted for r in recs])
+    np.savez_compressed(OUT / "c5_wedge.npz", **out)
+    print("c5_wedge.npz written")
+
+
 def fileio_fixtures():
     """Files written by the reference's fileio (tests/golden/fileio/): raw arrays with
     sidecars, a plan and its parse, a convergence CSV and a PGM preview."""
@@ -369,6 +406,8 @@ if __name__ == "__main__":
         c2_full()
     elif "--only-c3" in sys.argv:
         c3_chain()
+    elif "--only-c5" in sys.argv:
+        c5_wedge()
     else:
         main()
         c2_reduced()

@@ -112,6 +112,33 @@ def test_c3_chain_stated_size(tf):
         assert L == pytest.approx(float(d["lipschitz"][lvl]), rel=1e-3)
 
 
+def test_c5_wedge_fbp_vs_zero_init(tf):
+    """C5 geometry at reduced size (configs[4]): 4 x 320^2, 120 angles in [0, 2 pi/3),
+    30 iterations from FBP and from zero vs the reference (make_golden.py c5_wedge, the
+    reference's bench_init comparison, bench.py:108-131): reconstructions, fidelity
+    curves and restart flags; FBP starts from (and stays at) the lower residual."""
+    d = golden("c5_wedge.npz")
+    g = d["g"].astype(np.float64)
+    n = 320
+    p = _plan(tf, d["angles"], g.shape[2], n)
+    sino = tf.Sinogram(angles=d["angles"], data=g)
+    f_fbp = tf.fbp(p, sino)
+    assert 0.1 * float(f_fbp.data.max() - f_fbp.data.min()) == pytest.approx(float(d["sigma"]),
+                                                                             rel=1e-4)
+    ctx = tf.fidelity_context(p, tf.build_psf(p.sampling, n), sino)
+    prm = tf.QggmrfParams(sigma=float(d["sigma"]), lam=5e-4)
+    cfg = tf.SolverConfig(max_iters=30, tol=1e-300, lipschitz=float(d["L"]))
+    fid = {}
+    for name, f0 in (("fbp", f_fbp), ("zero", tf.Volume(np.zeros((4, n, n))))):
+        rec, recs = tf.solve(ctx, prm, cfg, f0)
+        assert rel_l2(rec.data, d[f"recon_{name}"]) < 1e-3
+        assert [r.restarted for r in recs] == list(d[f"restarted_{name}"])
+        fid[name] = np.array([r.fidelity for r in recs])
+        np.testing.assert_allclose(fid[name], d[f"fidelity_{name}"], rtol=1e-4,
+                                   atol=1e-4 * abs(d[f"fidelity_{name}"][0]))
+    assert fid["fbp"][0] < fid["zero"][0] and fid["fbp"][-1] < fid["zero"][-1]
+
+
 @pytest.mark.parametrize("n", [640, 1280])
 def test_wedge_apply_vs_oracle(tf, n):
     """C5 geometry: 120 angles uniform in [0, 2 pi / 3) (limited-angle wedge), Nd = N."""
