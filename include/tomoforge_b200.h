@@ -234,6 +234,18 @@ int tf_resample_axis(const float* d_in, float* d_out, long long outer, int n_src
                      long long inner, const int* d_start, const float* d_weights, int taps,
                      void* stream);
 
+/* All three axes of multires.upsample (multires.py:167-195) in one pass (K9f):
+ *   d_out[tz][i][j] = sum_{a,b,c} wz[t][a] wx[i][b] wy[j][c]
+ *                      d_src[sz[t]+a][sx[i]+b][sy[j]+c],   t = t_begin + tz,
+ * for tz < nzt, i < ht, j < wt; d_src is [zs][hs][ws] fp32.  Each band (start
+ * int32 [n_tgt], weights fp32 [n_tgt][k], k <= 8) is the reference matrix's
+ * edge-clamped, row-normalised band (as tf_resample_axis).  Upsampling only
+ * (hs <= ht, ws <= wt); a slab of the target is [t_begin, t_begin + nzt). */
+int tf_upsample3(const float* d_src, int zs, int hs, int ws, float* d_out, int t_begin, int nzt,
+                 int ht, int wt, const int* d_sz, const float* d_wz, int kz, const int* d_sx,
+                 const float* d_wx, int kx, const int* d_sy, const float* d_wy, int ky,
+                 void* stream);
+
 /* Per-kernel CUDA-event timing used by bench.py for the roofline numbers.
  * Enable (clears totals), run, then collect: ms_out[slot] = total ms and
  * n_out[slot] = launches per slot (0 k_rows_fwd, 1 k_cols_conv, 2 k_rows_inv). */
