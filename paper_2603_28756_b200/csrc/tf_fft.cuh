@@ -16,8 +16,16 @@
 // the outputs is needed; the first/last butterflies are pruned accordingly.
 //
 // Forward = e^{-2 pi i jk/M} (numpy.fft sign); INV = conjugate, unnormalised.
-// Twiddles: fp32 table of e^{-2 pi i j/TW_MAX} built in fp64 once per device
-// (tf_init); powers w^r by a log-depth product tree (error ~log2 R ulp).
+// Twiddles: fp32 per-length tables e^{-2 pi i j/L} built in fp64 once per device
+// (tf_init).  A pass's butterfly needs only its base twiddle w (one table word)
+// and the squares w^2, w^4, w^8 (dft_fold below).
+//
+// Butterflies (dft_fold): a radix-R pass computes X[q] = sum_r u_r w^r W_R^{rq}
+// as log2 R levels of radix-2 DIT steps, Z[q] = E + t O, Z[q + n/2] = 2E - Z[q],
+// with the external twiddle folded into each step's t = w^{R/n} W_n^q.  On the
+// paired-fp32 datapath that is 3 instructions per butterfly (two FFMA2 for
+// E + t O, one FFMA2 for 2E - Z) instead of a complex multiply per input plus
+// two FADD2 -- about 20 % fewer FP instructions per twiddled radix-16 pass.
 #pragma once
 #include "tf_complex.cuh"
 
@@ -27,16 +35,9 @@ constexpr int TW_MAX = 16384;  // largest supported transform length
 // Concatenated per-length tables: W_L^j = e^{-2 pi i j/L} at word (L - 2) + j for
 // L = 2, 4, ..., TW_MAX, so the twiddles of one pass are contiguous in k.
 constexpr int TW_WORDS = 2 * TW_MAX - 2;
-// Direct power tables for radix-16 passes (TwDirect): for NS in {2,4,8,16}
-// the powers W_{16 NS}^{k r} laid out [r][k] at tws_base(NS); for the M = 4096
-// last pass (NS = 256, k = t) the powers W_4096^{t r} laid out [r-1][t].
-constexpr int TWS_WORDS = 16 * 31;
-__host__ __device__ constexpr int tws_base(int ns) { return 16 * (ns - 1); }
 // one copy per translation unit (internal linkage, no relocatable device code);
 // every TU that runs FFTs fills its copy from ensure_init() via init_twiddles_tu()
 static __device__ c32 g_twiddle[TW_WORDS];
-static __device__ c32 g_tw_small[TWS_WORDS];
-static __device__ c32 g_tw_t256[15 * 256];
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 __host__ __device__ constexpr int pad_idx(int i) { return i + (i >> 4); }
@@ -53,115 +54,94 @@ __device__ __forceinline__ c32 tw_w(int k) {
   return g_twiddle[(L - 2) + k];
 }
 
-// --------------------------------------------------------------- codelets
-// In-place DFT of u[0..R-1]; output X[k] in u[k].  ZIN: u[R/2..R-1] == 0 on
-// entry (not read).  HOUT: only X[0..R/2-1] are produced.
-
-template <bool INV, bool ZIN = false, bool HOUT = false>
-__device__ __forceinline__ void dft4(c32& u0, c32& u1, c32& u2, c32& u3) {
-  c32 t0, t1, t2, t3;
-  if constexpr (ZIN) {
-    t0 = u0; t1 = u0; t2 = u1; t3 = rot_q<INV>(u1);
-  } else {
-    t0 = cadd(u0, u2); t1 = csub(u0, u2);
-    t2 = cadd(u1, u3); t3 = rot_q<INV>(csub(u1, u3));
-  }
-  u0 = cadd(t0, t2);
-  u1 = cadd(t1, t3);
-  if constexpr (!HOUT) {
-    u2 = csub(t0, t2);
-    u3 = csub(t1, t3);
-  }
-}
-
 constexpr float kH = 0.70710678118654752440f;  // 1/sqrt 2
 
-template <bool INV>
-__device__ __forceinline__ c32 w8_1(c32 a) { return rot_e<INV>(a, kH); }  // e^{-+i pi/4}
-template <bool INV>
-__device__ __forceinline__ c32 w8_3(c32 a) {                           // e^{-+3i pi/4}
-  const c32 p = pmul(a, mk(-kH, -kH));
-  return INV ? pfma(mk(a.y, a.x), mk(-kH, kH), p) : pfma(mk(a.y, a.x), mk(kH, -kH), p);
+// ---------------------------------------------------- FMA-folded codelet
+// cos(2 pi q / 16); W_16^q = (cos16(q), -cos16(q - 4)).  q is a constant after
+// unrolling, so the lookup folds to an immediate.
+__device__ __forceinline__ float cos16(int q) {
+  constexpr float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;
+  const float c[16] = {1.f, c1, kH, s1, 0.f, -s1, -kH, -c1, -1.f, -c1, -kH, -s1, 0.f, s1, kH, c1};
+  return c[q & 15];
 }
 
-template <bool INV, bool ZIN = false, bool HOUT = false>
-__device__ __forceinline__ void dft8(c32 (&u)[8]) {
-  c32 a[4], b[4];
+// e + o t (forward) or e + o conj(t) (INV): two FFMA2
+template <bool INV>
+__device__ __forceinline__ c32 cfma(c32 e, c32 o, c32 t) {
+  const c32 p = pfma(o, mk(t.x, t.x), e);
+  return INV ? pfma(mk(o.y, o.x), mk(t.y, -t.y), p) : pfma(mk(o.y, o.x), mk(-t.y, t.y), p);
+}
+// 2e - z: one FFMA2 (the partner output of a folded radix-2 step)
+__device__ __forceinline__ c32 twice_minus(c32 e, c32 z) {
+  return pfma(e, mk(2.f, 2.f), mk(-z.x, -z.y));
+}
+
+// In-place X[q] = sum_r u_r w^r W_R^{rq} (TW; else w = 1), conjugated for INV,
+// output X[q] in u[q].  pw[j] = w^{2^j}.  Radix-2 DIT over r: with Z_{r0,s} the
+// (R/s)-point twiddled DFT of u_{r0 + s j},
+//   Z_{r0,s}[q] = Z_{r0,2s}[q] + t Z_{r0+s,2s}[q],  Z_{r0,s}[q + n/2] = 2 Z_{r0,2s}[q] - Z_{r0,s}[q],
+// t = w^s W_n^q, n = R/s; Z_{r0,s}[q] lives at position r0 + s q.  Steps whose t
+// is 1 or -i (no TW) are two FADD2; all others three FFMA2.  ZIN: u[R/2..] == 0
+// (not read); HOUT: only X[0..R/2-1] are produced.
+// one radix-2 level (n = 2^LV) of dft_fold: a -> b
+template <int R, int LV, bool INV, bool ZIN, bool HOUT, bool TW>
+__device__ __forceinline__ void fold_level(const c32 (&a)[R], c32 (&b)[R], const c32* pw) {
+  constexpr int LR = ilog2(R);
+  constexpr int n = 1 << LV, s = R >> LV, h = n >> 1, nq = n >= 4 ? n / 4 : 1;
+  constexpr bool last = LV == LR;
+  c32 ws = mk(1.f, 0.f);
+  c32 tq[nq];  // w^s W_n^{q'}, 0 < q' < n/4
+  if constexpr (TW) {
+    ws = pw[LR - LV];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if constexpr (ZIN) {
-      a[k] = u[k]; b[k] = u[k];
-    } else {
-      a[k] = cadd(u[k], u[k + 4]); b[k] = csub(u[k], u[k + 4]);
+    for (int qp = 1; qp < nq; ++qp)
+      tq[qp] = cmul(ws, mk(cos16(qp * 16 / n), -cos16(qp * 16 / n - 4)));
+  }
+#pragma unroll
+  for (int r0 = 0; r0 < s; ++r0) {
+#pragma unroll
+    for (int q = 0; q < h; ++q) {
+      const int pos0 = r0 + s * q, pos1 = pos0 + R / 2;
+      const c32 e = a[r0 + 2 * s * q];
+      if constexpr (ZIN && LV == 1) {
+        b[pos0] = e;
+        b[pos1] = e;
+      } else {
+        const c32 o = a[r0 + s + 2 * s * q];
+        const int qp = q % nq;
+        const bool quarter = n >= 4 && q >= nq;
+        if (!TW && qp == 0) {
+          const c32 to = quarter ? rot_q<INV>(o) : o;
+          b[pos0] = cadd(e, to);
+          if constexpr (!(HOUT && last)) b[pos1] = csub(e, to);
+        } else {
+          c32 t = qp == 0 ? ws
+                  : TW    ? tq[qp]
+                          : mk(cos16(qp * 16 / n), -cos16(qp * 16 / n - 4));
+          if (quarter) t = mk(t.y, -t.x);  // -i t
+          const c32 z = cfma<INV>(e, o, t);
+          b[pos0] = z;
+          if constexpr (!(HOUT && last)) b[pos1] = twice_minus(e, z);
+        }
+      }
     }
   }
-  b[1] = w8_1<INV>(b[1]);
-  b[2] = rot_q<INV>(b[2]);
-  b[3] = w8_3<INV>(b[3]);
-  dft4<INV, false, HOUT>(a[0], a[1], a[2], a[3]);
-  dft4<INV, false, HOUT>(b[0], b[1], b[2], b[3]);
+}
+
+template <int R, int LV, bool INV, bool ZIN, bool HOUT, bool TW>
+__device__ __forceinline__ void fold_levels(c32 (&a)[R], const c32* pw) {
+  if constexpr (LV <= ilog2(R)) {
+    c32 b[R];
+    fold_level<R, LV, INV, ZIN, HOUT, TW>(a, b, pw);
+    fold_levels<R, LV + 1, INV, ZIN, HOUT, TW>(b, pw);
 #pragma unroll
-  for (int m = 0; m < (HOUT ? 2 : 4); ++m) {
-    u[2 * m] = a[m];
-    u[2 * m + 1] = b[m];
+    for (int r = 0; r < R; ++r) a[r] = b[r];
   }
 }
 
-template <bool INV>
-__device__ __forceinline__ c32 w16(c32 a, int e) {  // a * W16^e for e in {1,2,3,4,6,9}
-  const float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;
-  switch (e) {
-    case 1: return INV ? cmul(a, mk(c1, s1)) : cmul(a, mk(c1, -s1));
-    case 2: return w8_1<INV>(a);
-    case 3: return INV ? cmul(a, mk(s1, c1)) : cmul(a, mk(s1, -c1));
-    case 4: return rot_q<INV>(a);
-    case 6: return w8_3<INV>(a);
-    default: return INV ? cmul(a, mk(-c1, -s1)) : cmul(a, mk(-c1, s1));  // 9
-  }
-}
-
-template <bool INV, bool ZIN = false, bool HOUT = false>
-__device__ __forceinline__ void dft16(c32 (&u)[16]) {
-  // 16 = 4 x 4: DFT4 over l of u[k + 4l], twiddle W16^{km}, DFT4 over k -> X[m + 4j]
-  c32 y[4][4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    c32 a0 = u[k], a1 = u[k + 4], a2, a3;
-    if constexpr (!ZIN) { a2 = u[k + 8]; a3 = u[k + 12]; }
-    dft4<INV, ZIN>(a0, a1, a2, a3);
-    y[k][0] = a0; y[k][1] = a1; y[k][2] = a2; y[k][3] = a3;
-  }
-#pragma unroll
-  for (int k = 1; k < 4; ++k)
-#pragma unroll
-    for (int m = 1; m < 4; ++m) y[k][m] = w16<INV>(y[k][m], k * m);
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    c32 a0 = y[0][m], a1 = y[1][m], a2 = y[2][m], a3 = y[3][m];
-    dft4<INV, false, HOUT>(a0, a1, a2, a3);
-    u[m] = a0; u[m + 4] = a1;
-    if constexpr (!HOUT) { u[m + 8] = a2; u[m + 12] = a3; }
-  }
-}
-
-template <int R, bool INV, bool ZIN, bool HOUT>
-__device__ __forceinline__ void dft(c32 (&u)[R]) {
-  if constexpr (R == 1) {
-  } else if constexpr (R == 2) {
-    if constexpr (ZIN) {
-      u[1] = u[0];
-    } else {
-      const c32 s = cadd(u[0], u[1]), d = csub(u[0], u[1]);
-      u[0] = s; u[1] = d;
-    }
-  } else if constexpr (R == 4) {
-    dft4<INV, ZIN, HOUT>(u[0], u[1], u[2], u[3]);
-  } else if constexpr (R == 8) {
-    dft8<INV, ZIN, HOUT>(u);
-  } else {
-    static_assert(R == 16, "radix");
-    dft16<INV, ZIN, HOUT>(u);
-  }
+template <int R, bool INV, bool ZIN, bool HOUT, bool TW>
+__device__ __forceinline__ void dft_fold(c32 (&u)[R], const c32* pw) {
+  fold_levels<R, 1, INV, ZIN, HOUT, TW>(u, pw);
 }
 
 // --------------------------------------------------------------- engine
@@ -189,71 +169,33 @@ __device__ __forceinline__ int canon_word(int t, int m) {
   else return pad_idx(t + T * m);
 }
 
-// Forward twiddles of pass P for thread t: wp[i][r] = w_i^r, w_i = e^{-2 pi i k_i/(NS R)},
-// k_i = (t + i T) mod NS, from the per-length table and a log-depth product tree.
+// Forward twiddle powers of pass P for thread t: p[i][j] = w_i^{2^j},
+// w_i = e^{-2 pi i k_i/(NS R)}, k_i = (t + i T) mod NS.
 template <int M, int E, int P>
 struct PassTw {
   using S = FftShape<M, E>;
-  static constexpr int R = 1 << S::lradix(P);
+  static constexpr int LR = S::lradix(P);
+  static constexpr int R = 1 << LR;
   static constexpr int NS = S::ns(P);
   static constexpr int ST = E / R;
-  c32 w[ST][R];
-  // table entry W^k + log-depth product tree for the other powers (FP work)
+  c32 p[ST][LR > 0 ? LR : 1];
+  // base twiddle from the table, its powers by squaring (FP work)
   __device__ __forceinline__ void from_table(int t) {
 #pragma unroll
     for (int i = 0; i < ST; ++i) {
       const int k = (t + i * S::T) & (NS - 1);
-      w[i][1] = tw_w<NS * R>(k);
+      p[i][0] = tw_w<NS * R>(k);
 #pragma unroll
-      for (int r = 2; r < R; ++r) w[i][r] = cmul(w[i][r / 2], w[i][r - r / 2]);
-    }
-  }
-  // every power straight from a table where one exists (memory instead of FP
-  // work; used by the FMA-bound column kernel): [r][k] tables for NS <= 16 and
-  // the per-thread [r][t] table of the M = 4096 last pass
-  __device__ __forceinline__ void from_table_direct(int t) {
-#pragma unroll
-    for (int i = 0; i < ST; ++i) {
-      const int k = (t + i * S::T) & (NS - 1);
-      if constexpr (R == 16 && NS >= 2 && NS <= 16) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) w[i][r] = g_tw_small[tws_base(NS) + r * NS + k];
-      } else if constexpr (R == 16 && NS == 256 && S::T == 256) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) w[i][r] = __ldg(g_tw_t256 + (r - 1) * 256 + k);
-      } else {
-        w[i][1] = tw_w<NS * R>(k);
-#pragma unroll
-        for (int r = 2; r < R; ++r) w[i][r] = cmul(w[i][r / 2], w[i][r - r / 2]);
-      }
+      for (int j = 1; j < LR; ++j) p[i][j] = cmul(p[i][j - 1], p[i][j - 1]);
     }
   }
 };
 
-// default twiddle source: table + product tree
+// default twiddle source: table + squaring
 struct TwTable {
   template <int M, int E, int P>
   __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
     tw.from_table(t);
-  }
-};
-
-// small [r][k] power tables where NS <= 16 (L1-resident, 2 KB), product tree for
-// the per-thread last-pass powers (whose 30 KB table would live in L2)
-struct TwMixed {
-  template <int M, int E, int P>
-  __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
-    using PT = PassTw<M, E, P>;
-    if constexpr (PT::R == 16 && PT::NS >= 2 && PT::NS <= 16) tw.from_table_direct(t);
-    else tw.from_table(t);
-  }
-};
-
-// direct power tables (see PassTw::from_table_direct)
-struct TwDirect {
-  template <int M, int E, int P>
-  __device__ __forceinline__ void operator()(PassTw<M, E, P>& tw, int t) const {
-    tw.from_table_direct(t);
   }
 };
 
@@ -269,12 +211,8 @@ __device__ __forceinline__ void fft_pass(c32 (&v)[NB][E], const PassTw<M, E, P>*
       c32 u[R];
 #pragma unroll
       for (int r = 0; r < (ZIN ? R / 2 : R); ++r) u[r] = v[b][i + r * ST];
-      if constexpr (P > 0 && R > 1) {
-#pragma unroll
-        for (int r = 1; r < (ZIN ? R / 2 : R); ++r)
-          u[r] = INV ? cmulc(u[r], tw->w[i][r]) : cmul(u[r], tw->w[i][r]);
-      }
-      dft<R, INV, ZIN, HOUT>(u);
+      if constexpr (P > 0 && R > 1) dft_fold<R, INV, ZIN, HOUT, true>(u, tw->p[i]);
+      else dft_fold<R, INV, ZIN, HOUT, false>(u, nullptr);
 #pragma unroll
       for (int r = 0; r < (HOUT ? R / 2 : R); ++r) v[b][i + r * ST] = u[r];
     }
@@ -312,7 +250,7 @@ __device__ __forceinline__ void load_canonical(c32 (&v)[NB][E], const c32* sm, i
 
 // Pass P with its twiddles already in `tw` (null for P = 0).  The twiddles of
 // pass P+1 are fetched *before* the exchange that precedes it, so their loads
-// (or product-tree FMAs) overlap the shared-memory round trip and the barrier
+// (and squarings) overlap the shared-memory round trip and the barrier
 // instead of stalling the next pass (TF_TW_EARLY = 0 restores in-place fetches).
 #ifndef TF_TW_EARLY
 #define TF_TW_EARLY 1
@@ -388,33 +326,12 @@ static __global__ void k_twiddle_init(c32* tw) {
   tw[w] = mk((float)c, (float)s);
 }
 
-static __global__ void k_twiddle_init_small(c32* small, c32* t256) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  double s, c;
-  if (w < TWS_WORDS) {
-    int ns = 1;
-    while (w >= tws_base(2 * ns)) ns *= 2;  // segment [tws_base(ns), tws_base(2 ns))
-    const int e = w - tws_base(ns), r = e / ns, k = e - r * ns;
-    const int L = 16 * ns;
-    sincospi(-2.0 * (double)((k * r) % L) / L, &s, &c);
-    small[w] = mk((float)c, (float)s);
-  }
-  if (w < 15 * 256) {
-    const int r = w / 256 + 1, t = w % 256;
-    sincospi(-2.0 * (double)((t * r) % 4096) / 4096.0, &s, &c);
-    t256[w] = mk((float)c, (float)s);
-  }
-}
-
 // fill this translation unit's tables on the current device (synchronous)
 static inline cudaError_t init_twiddles_tu() {
-  c32 *p = nullptr, *q = nullptr, *u = nullptr;
+  c32* p = nullptr;
   cudaError_t e = cudaGetSymbolAddress((void**)&p, g_twiddle);
-  if (e == cudaSuccess) e = cudaGetSymbolAddress((void**)&q, g_tw_small);
-  if (e == cudaSuccess) e = cudaGetSymbolAddress((void**)&u, g_tw_t256);
   if (e != cudaSuccess) return e;
   k_twiddle_init<<<(TW_WORDS + 255) / 256, 256>>>(p);
-  k_twiddle_init_small<<<(15 * 256 + 255) / 256, 256>>>(q, u);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return cudaDeviceSynchronize();

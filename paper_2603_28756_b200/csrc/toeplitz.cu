@@ -430,8 +430,8 @@ k_cols_conv(c32* __restrict__ T, const c32* __restrict__ PQ, const float* __rest
   }
 }
 
-// twiddles of the column kernel: table entry + product tree (table-loaded powers
-// measured slower: the last-pass table lives in L2)
+// twiddles of the column kernel: one table entry per pass + squarings (a 2 KB
+// pass-1 table and a 30 KB last-pass table measured slower)
 using K2Tw = TwTable;
 
 // K2 for 1024 <= M <= 4096: a persistent, TMA-fed column kernel.  Each CTA walks
