@@ -713,7 +713,7 @@ def _c5(args, world, rank):
     [0, 2 pi / 3) wedge, Nd = 2560, noise rms 0.5; the 3-level (640, 1280, 2560)
     schedule from FBP and from zero (the reference's bench_init comparison,
     bench.py:108-131) -- fidelity per iteration for both inits.
-    N = 2560 runs on the power-of-two FFT grid M = 8192 (no radix-5 passes)."""
+    The levels run on the radix-5 FFT sides M = 1280 / 2560 / 5120 (toeplitz5.cu)."""
     import torch
 
     import paper_2603_28756_b200 as tf
@@ -745,8 +745,8 @@ def _c5(args, world, rank):
     prm = tf.QggmrfParams(sigma=0.1, lam=5e-4)
     out = {"config": f"C5: {n}^2 x {z} 3-D Shepp-Logan, {n_ang} angles in [0, 2pi/3), Nd={nd}, "
                      f"noise rms 0.5, levels {hier.levels} x {hier.iters_per_level}, qGGMRF "
-                     "sigma=0.1 lam=5e-4, per-level power-iteration L; FFT grid 8192 at the "
-                     "finest level", "n_gpus": world}
+                     "sigma=0.1 lam=5e-4, per-level power-iteration L; FFT grids "
+                     f"{[tf.fft_side_for(s) for s in hier.levels]}", "n_gpus": world}
     for name, fbp_init in (("fbp", True), ("zero", False)):
         torch.cuda.synchronize()
         barrier(world)

@@ -67,6 +67,7 @@ static std::vector<int> g_sms;
 
 int init_twiddles_toeplitz();
 int init_twiddles_nufft();
+int init_twiddles_toeplitz5();
 
 int ensure_init() {
   int dev = 0;
@@ -79,6 +80,7 @@ int ensure_init() {
   if (!g_inited[dev]) {
     TF_TRY(init_twiddles_toeplitz());
     TF_TRY(init_twiddles_nufft());
+    TF_TRY(init_twiddles_toeplitz5());
     int sms = 0;
     TF_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev),
                       "cudaDeviceGetAttribute"));
@@ -164,6 +166,9 @@ int tf_fft_side(int n) {
   int M = 8;
   while (M < 2 * n - 1) M <<= 1;
   if (M > 8192) return fail_arg("source side %d exceeds the supported maximum 4096", n);
+  // a 5 * 2^k side (radix-5 step, toeplitz5.cu) when it is smaller
+  for (int q = 256; q <= 1024; q <<= 1)
+    if (5 * q >= 2 * n - 1 && 5 * q < M) return 5 * q;
   return M;
 }
 
@@ -177,7 +182,8 @@ long long tf_psf_workspace_bytes(int M) { return (long long)psf_workspace_bytes(
 int tf_psf_build(int n, int M, int n_angles, const double* d_cossin, int nd, void* d_PQ,
                  float* d_Bi, void* d_ws, long long ws_bytes, void* stream) {
   TF_TRY(ensure_init());
-  if (n < 1 || M < 2 * n - 1 || !is_pow2(M)) return fail_arg("bad psf sides n=%d M=%d", n, M);
+  if (n < 1 || M < 2 * n - 1 || !(is_pow2(M) || is_side5(M)))
+    return fail_arg("bad psf sides n=%d M=%d", n, M);
   if (n_angles < 1 || nd < 1) return fail_arg("bad sampling (angles=%d, nd=%d)", n_angles, nd);
   if (!d_cossin || !d_PQ || !d_Bi || !d_ws) return fail_arg("null pointer");
   return psf_build(n, M, d_cossin, n_angles, nd, d_PQ, d_Bi, d_ws, (size_t)ws_bytes,
@@ -198,7 +204,8 @@ int tf_toeplitz_apply(const float* d_x, float* d_out, const float* d_aux, float 
                       const float* d_Bi, int has_flip, void* d_ws, long long ws_bytes,
                       void* stream) {
   TF_TRY(ensure_init());
-  if (n < 1 || M < 2 * n - 1 || !is_pow2(M)) return fail_arg("bad sides n=%d M=%d", n, M);
+  if (n < 1 || M < 2 * n - 1 || !(is_pow2(M) || is_side5(M)))
+    return fail_arg("bad sides n=%d M=%d", n, M);
   if (nslices < 0) return fail_arg("negative slice count");
   if (nslices == 0) return TF_OK;
   if (!d_x || !d_out || !d_PQ || (has_flip && !d_Bi) || !d_ws)

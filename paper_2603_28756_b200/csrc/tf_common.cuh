@@ -31,6 +31,17 @@ void timer_end(KernelTimer& t);
 
 inline bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
 
+// M = 5Q FFT sides (toeplitz5.cu): Toeplitz apply and PSF build
+bool is_side5(int M);
+int toeplitz_apply5(const float* x, float* out, const float* aux, float alpha, float beta,
+                    long long nslices, int n, int M, const void* PQ, const float* Bi, bool flip,
+                    void* ws, size_t ws_bytes, cudaStream_t st);
+int psf_build5(int n, int M, const double* cs, int n_angles, int nd, void* PQ, float* Bi,
+               void* ws, cudaStream_t st);
+// K6 lag kernels on the M x M grid (toeplitz.cu)
+int psf_lags_launch(float* lags, int n, int M, const double* cs, int n_angles, int nd,
+                    cudaStream_t st);
+
 // opt a kernel into more than 48 KB of dynamic shared memory
 template <typename K>
 inline int prep_kernel(K kern, size_t smem) {

@@ -927,12 +927,7 @@ struct PsfFn {
     c32* T = reinterpret_cast<c32*>(ws + 2 * MM * sizeof(float));
     c32* spec = T + 2 * H * M;
     const bool flip = (nd % 2) == 0;
-    {
-      const int bs = 256;
-      const long long nb = (MM + bs - 1) / bs;
-      k_psf_lags<<<(unsigned)nb, bs, 0, st>>>(lags, lags + MM, n, M, cs, n_angles, nd);
-      TF_TRY(check_launch("k_psf_lags"));
-    }
+    TF_TRY(psf_lags_launch(lags, n, M, cs, n_angles, nd, st));
     TF_TRY(launch_rows_fwd<M>(lags, T, M, M, MM, M, flip ? 2 : 1, st));
     TF_TRY(launch_cols_fwd<M>(T, spec, M, flip ? 2 : 1, st));
     {
@@ -959,6 +954,15 @@ struct SpectrumFn {
 
 }  // namespace
 
+int psf_lags_launch(float* lags, int n, int M, const double* cs, int n_angles, int nd,
+                    cudaStream_t st) {
+  const long long MM = (long long)M * M;
+  const int bs = 256;
+  k_psf_lags<<<(unsigned)((MM + bs - 1) / bs), bs, 0, st>>>(lags, lags + MM, n, M, cs, n_angles,
+                                                             nd);
+  return check_launch("k_psf_lags");
+}
+
 size_t spectrum_workspace_bytes(int n, int M) {
   return (size_t)(M / 2 + 1) * RB * nrb_of(n) * sizeof(c32);  // row pass output per slice
 }
@@ -973,6 +977,8 @@ int real_spectrum(const float* img, long long nslices, int n, int M, void* T, vo
 int toeplitz_apply(const float* x, float* out, const float* aux, float alpha, float beta,
                    long long nslices, int n, int M, const void* PQ, const float* Bi, bool flip,
                    void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (is_side5(M))
+    return toeplitz_apply5(x, out, aux, alpha, beta, nslices, n, M, PQ, Bi, flip, ws, ws_bytes, st);
   const long long per = (long long)(M / 2 + 1) * RB * nrb_of(n) * (long long)sizeof(c32);
   const long long chunk = (long long)(ws_bytes / per);
   if (chunk < 1) return fail_arg("toeplitz workspace too small: %zu < %lld", ws_bytes, per);
@@ -989,6 +995,7 @@ size_t psf_workspace_bytes(int M) {
 int psf_build(int n, int M, const double* cs, int n_angles, int nd, void* PQ, float* Bi,
               void* ws, size_t ws_bytes, cudaStream_t st) {
   if (ws_bytes < psf_workspace_bytes(M)) return fail_arg("psf workspace too small");
+  if (is_side5(M)) return psf_build5(n, M, cs, n_angles, nd, PQ, Bi, ws, st);
   return dispatch_m<PsfFn>(M, n, cs, n_angles, nd, reinterpret_cast<c32*>(PQ), Bi,
                            reinterpret_cast<char*>(ws), st);
 }

@@ -44,6 +44,8 @@ def test_host_only_entry_points(lib):
     lib.tf_fft_side.restype = ctypes.c_int
     assert lib.tf_fft_side(2048) == 4096
     assert lib.tf_fft_side(256) == 512
+    # 5 * 2^k sides where smaller (radix-5 step): the C5 levels 640 / 1280 / 2560
+    assert [lib.tf_fft_side(n) for n in (640, 1280, 2560, 600, 300)] == [1280, 2560, 5120, 1280, 1024]
     assert lib.tf_fft_side(0) == -1
     lib.tf_last_error.restype = ctypes.c_char_p
     assert b"positive" in lib.tf_last_error()

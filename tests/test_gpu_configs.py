@@ -156,13 +156,14 @@ def test_wedge_apply_vs_oracle(tf, n):
 
 @pytest.mark.parametrize("n", [2560, 4096])
 def test_large_sides_operator_properties(tf, n):
-    """C5 slice side (M = 8192) and the maximum side: K is linear, self-adjoint, PSD."""
+    """C5 slice side (M = 5120, radix-5 step) and the maximum side (M = 8192): K is
+    linear, self-adjoint, PSD."""
     import torch
 
     ang = np.linspace(0.0, np.pi, 64, endpoint=False)
     geom = tf.ScanGeometry(angles=ang, detector_bins=n, image_side=n)
     psf = tf.build_psf(tf.polar_sampling(geom), n)
-    assert psf.fft_side == 8192
+    assert psf.fft_side == (5120 if n == 2560 else 8192)
     gen = torch.Generator(device="cuda").manual_seed(n)
     x = torch.randn((1, n, n), device="cuda", generator=gen, dtype=torch.float32)
     y = torch.randn((1, n, n), device="cuda", generator=gen, dtype=torch.float32)

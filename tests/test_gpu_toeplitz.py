@@ -87,14 +87,43 @@ def test_size_mismatch(tf):
         tf.toeplitz_apply(psf, np.zeros((8, 8)))
 
 
-@pytest.mark.parametrize("n,n_ang,nd", [(256, 90, 256), (512, 90, 1024), (200, 33, 201)])
+@pytest.mark.parametrize("n,n_ang,nd", [(256, 90, 256), (512, 90, 1024), (200, 33, 201),
+                                         (640, 60, 640), (600, 45, 601), (1280, 90, 1280)])
 def test_apply_vs_oracle_midsize(tf, n, n_ang, nd):
+    """Power-of-two sides and the 5 * 2^k sides of the radix-5 path (640, 600 -> 1280,
+    1280 -> 2560)."""
     import oracle as O
 
     ang = np.linspace(0, np.pi, n_ang, endpoint=False)
     x = np.random.default_rng(n).standard_normal((2, n, n))
     ref = O.apply_batch(O.build_psf(ang, nd, n), x)
-    out = tf.toeplitz_apply(_psf(tf, ang, nd, n), x)
+    psf = _psf(tf, ang, nd, n)
+    assert psf.fft_side == _lib_side(n)
+    out = tf.toeplitz_apply(psf, x)
+    assert rel_l2(out, ref) < 1e-5
+
+
+def _lib_side(n):
+    m = 1
+    while m < 2 * n - 1:
+        m *= 2
+    five = [5 * q for q in (256, 512, 1024) if 2 * n - 1 <= 5 * q < m]
+    return five[0] if five else m
+
+
+@pytest.mark.parametrize("nd", [2560, 2561])
+def test_apply_2560_wedge_vs_oracle(tf, nd):
+    """The C5 slice (configs[4]): one 2560^2 slice, 120 angles over a 120-degree wedge,
+    on the radix-5 side M = 5120; Nd even (flip term) and odd."""
+    import oracle as O
+
+    n = 2560
+    ang = np.linspace(0, 2 * np.pi / 3, 120, endpoint=False)
+    x = np.random.default_rng(1).standard_normal((1, n, n))
+    ref = O.apply_batch(O.build_psf(ang, nd, n), x)
+    psf = _psf(tf, ang, nd, n)
+    assert psf.fft_side == 5120
+    out = tf.toeplitz_apply(psf, x)
     assert rel_l2(out, ref) < 1e-5
 
 

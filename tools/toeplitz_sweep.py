@@ -13,9 +13,9 @@ from paper_2603_28756_b200 import _lib  # noqa: E402
 from paper_2603_28756_b200.toeplitz import apply_stack  # noqa: E402
 
 z = int(os.environ.get("SWEEP_SLICES", "64"))
-n = 2048
+n = int(os.environ.get("SWEEP_N", "2048"))
 ang = np.linspace(0, np.pi, 128, endpoint=False)
-geom = tf.ScanGeometry(angles=ang, detector_bins=2048, image_side=n)
+geom = tf.ScanGeometry(angles=ang, detector_bins=n, image_side=n)
 psf = tf.build_psf(tf.polar_sampling(geom), n)
 x = torch.randn((z, n, n), device="cuda")
 rs = torch.randn((z, n, n), device="cuda")
@@ -37,6 +37,6 @@ for _ in range(steps):
 torch.cuda.synchronize()
 kt = {k: round(t / c, 4) for k, (t, c) in _lib.timing_collect().items()}
 _lib.timing_enable(False)
-print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("TF_")},
+print(json.dumps({"n": n, "fft_side": psf.fft_side, "env": {k: v for k, v in os.environ.items() if k.startswith("TF_")},
                   "ms_per_step": round(ms, 4), "evals_per_s": round(z / ms * 1e3, 1),
                   "kernel_ms": kt}))
