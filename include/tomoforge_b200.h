@@ -28,7 +28,8 @@ int tf_version(void);
 /* Build the per-device twiddle table on the current device (idempotent). */
 int tf_init(void);
 
-/* FFT side M used for an N x N source grid: the smallest power of two >= 2N-1.
+/* FFT side M used for an N x N source grid: the smallest M >= 2N-1 among the
+ * powers of two and 5 * 2^k (k = 8, 9, 10: a radix-5 step, e.g. N = 2560 -> 5120).
  * Replaces padded_side_for (toeplitz.py:53-60), which picks the smallest ODD
  * 7-smooth side; the even grid is exact for the re-embedded lag kernels
  * (DESIGN.md §3).  Returns M, or -1 for unsupported N (> 4096). */

@@ -58,7 +58,8 @@ def padded_side_for(source_side: int) -> int:
 
 
 def fft_side_for(source_side: int) -> int:
-    """FFT grid side used on the GPU: the smallest power of two >= 2N-1."""
+    """FFT grid side used on the GPU: the smallest M >= 2N-1 that is a power of two
+    or 5 * 2^k, k = 8..10 (radix-5 step: N = 640 / 1280 / 2560 -> 1280 / 2560 / 5120)."""
     m = _lib.load().tf_fft_side(int(source_side))
     if m < 0:
         _lib.check(m, "tf_fft_side")
