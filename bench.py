@@ -352,9 +352,11 @@ def run_ours(args, world, rank, local):
         "traffic": _ncu_traffic(dom),
         "ncu_pipes": _ncu_json("ncu_pipes.json", dom),
         "per_kernel": per_kernel,
-        "limiter_note": "k_cols_conv is FP32-FMA-pipe bound (ncu: FMA pipe ~67 %, top stall "
-                        "math-pipe throttle; DRAM bytes equal the algorithmic bytes); see "
-                        "DESIGN.md §3 and profiles/r01_ncu_kernels.txt",
+        "limiter_note": "k_cols_conv is bound by its FP32 pipe and its shared-memory exchanges "
+                        "together (ncu: FMA pipe 56 %, shared ld+st wavefronts 52 %, issue 43 %; "
+                        "DRAM bytes equal the algorithmic bytes; exchange-only variant 1.23 ms, "
+                        "FP-only variant 1.61 ms, full 1.99 ms); see DESIGN.md §3 and "
+                        "profiles/r02/ncu_kernels.txt",
         "gradient_total": {"bytes_per_eval": total_bytes / z,
                            "achieved": total_bytes / (tot_ms / 1e3) / 1e9,
                            "frac": total_bytes / (tot_ms / 1e3) / 1e9 / peak["value"]},

@@ -241,11 +241,13 @@ int tf_resample_axis(const float* d_in, float* d_out, long long outer, int n_src
  * for tz < nzt, i < ht, j < wt; d_src is [zs][hs][ws] fp32.  Each band (start
  * int32 [n_tgt], weights fp32 [n_tgt][k], k <= 8) is the reference matrix's
  * edge-clamped, row-normalised band (as tf_resample_axis).  Upsampling only
- * (hs <= ht, ws <= wt); a slab of the target is [t_begin, t_begin + nzt). */
+ * (hs <= ht, ws <= wt); a slab of the target is [t_begin, t_begin + nzt).
+ * win_rows / win_cols bound the coarse window of every 32 x 128 target tile
+ * (<= 40 / 136): the span of the tile's band starts plus the taps. */
 int tf_upsample3(const float* d_src, int zs, int hs, int ws, float* d_out, int t_begin, int nzt,
                  int ht, int wt, const int* d_sz, const float* d_wz, int kz, const int* d_sx,
                  const float* d_wx, int kx, const int* d_sy, const float* d_wy, int ky,
-                 void* stream);
+                 int win_rows, int win_cols, void* stream);
 
 /* Per-kernel CUDA-event timing used by bench.py for the roofline numbers.
  * Enable (clears totals), run, then collect: ms_out[slot] = total ms and

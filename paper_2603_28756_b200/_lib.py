@@ -60,7 +60,7 @@ _SIGNATURES = {
                                                            _c_double] + [_c_void_p] * 7),
     "tf_upsample3": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_int, _c_int, _c_int,
                               _c_int, _c_void_p, _c_void_p, _c_int, _c_void_p, _c_void_p, _c_int,
-                              _c_void_p, _c_void_p, _c_int, _c_void_p]),
+                              _c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_void_p]),
     "tf_solver_decide": (_c_int, [_c_void_p] * 4 + [_c_double, _c_int, _c_int, _c_double,
                                                     _c_void_p]),
     "tf_energy_fid": (_c_int, [_c_void_p] * 6 + [_c_int, _c_int, _c_int, _c_int, _c_int, _c_double,

@@ -139,7 +139,7 @@ int nufft_plan_weights(const double* kxy, long long S, int os, int w, double bet
                        float* wts, cudaStream_t st);
 int upsample3(const float* src, int zs, int hs, int ws, float* out, int t_begin, int nzt, int ht,
               int wt, const int* sz, const float* wz, int kz, const int* sx, const float* wx, int kx,
-              const int* sy, const float* wy, int ky, cudaStream_t st);
+              const int* sy, const float* wy, int ky, int nrm, int ncm, cudaStream_t st);
 int resample_axis(const float* in, float* out, long long outer, int n_src, int n_tgt,
                   long long inner, const int* s0, const float* w, int K, cudaStream_t st);
 int detector_rows(const float* rows, long long nrows, int nd, int n_angles, const void* sph,
@@ -413,7 +413,7 @@ int tf_direct_dft(const double* d_image, int n, const double* d_kxy, long long n
 int tf_upsample3(const float* d_src, int zs, int hs, int ws, float* d_out, int t_begin, int nzt,
                  int ht, int wt, const int* d_sz, const float* d_wz, int kz, const int* d_sx,
                  const float* d_wx, int kx, const int* d_sy, const float* d_wy, int ky,
-                 void* stream) {
+                 int win_rows, int win_cols, void* stream) {
   TF_TRY(ensure_init());
   if (zs < 1 || hs < 1 || ws < 1 || ht < 1 || wt < 1 || nzt < 0 || t_begin < 0)
     return fail_arg("bad upsample shapes");
@@ -421,7 +421,7 @@ int tf_upsample3(const float* d_src, int zs, int hs, int ws, float* d_out, int t
     return fail_arg("null pointer");
   if (d_src == d_out) return fail_arg("in-place resampling is not supported");
   return upsample3(d_src, zs, hs, ws, d_out, t_begin, nzt, ht, wt, d_sz, d_wz, kz, d_sx, d_wx, kx,
-                   d_sy, d_wy, ky, (cudaStream_t)stream);
+                   d_sy, d_wy, ky, win_rows, win_cols, (cudaStream_t)stream);
 }
 
 int tf_resample_axis(const float* d_in, float* d_out, long long outer, int n_src, int n_tgt,

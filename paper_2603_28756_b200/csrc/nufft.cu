@@ -25,7 +25,9 @@
 //                        CTA owns one tile for NB slices: lane = grid column,
 //                        each warp owns 4 grid rows, and every grid point is
 //                        accumulated by exactly one thread in sample order --
-//                        deterministic, no shared or global atomics.  The tile
+//                        deterministic, no shared or global atomics.  Samples
+//                        are staged 32 at a time per warp (one lane per
+//                        sample's index chain) in shared memory.  The tile
 //                        is stored with a per-index phase e^{-2 pi i a (N/2)/os} so
 //                        the centred N x N crop of the inverse FFT becomes its
 //                        first N outputs (pruned last pass).
@@ -165,16 +167,33 @@ __global__ void k_detector_rows(const float* __restrict__ rows, int nd, int L, i
 // Tile of 32 (a, lanes) x 32 (b, 4 per warp) grid points for NB slices.
 // ab[m] = (a0, b0): first grid index of sample m's window (mod os); wts[m] =
 // (wx[0..W), wy[0..W)); c: [nslices][c_stride] samples.
+//
+// Each warp walks its band list (the samples whose window touches its 4 rows,
+// sample order) in chunks of 32: lane l fetches the index chain tile_idx -> ab ->
+// weights / values of sample base + l (32 independent chains in flight instead of
+// one), the chunk is staged in the warp's shared-memory slot, and while the warp
+// accumulates it sample by sample from shared memory (broadcast reads), the next
+// chunk's fetches are already in flight.  Every grid point is still accumulated by
+// one thread in sample order with the same arithmetic: deterministic, no atomics.
+template <int W, int NB>
+struct SpreadStage {
+  int2 ab[32];
+  float w[32][2 * W + 1];  // +1: rows of odd stride (distinct banks per sample)
+  c32 cv[32][NB];
+};
+
 template <int W, int NB>
 __global__ void __launch_bounds__(256)
 k_spread(const c32* __restrict__ c, long long c_stride, int nslices, int os, int ntile_a,
          const int* __restrict__ tile_ptr, const int* __restrict__ tile_idx,
          const int2* __restrict__ ab, const float* __restrict__ wts, const c32* __restrict__ preph,
          c32* __restrict__ grid) {
+  __shared__ SpreadStage<W, NB> stage_all[8];
   const int tile = blockIdx.x;
   const int ta = tile % ntile_a, tb = tile / ntile_a;
   const int z0 = blockIdx.y * NB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  SpreadStage<W, NB>& st = stage_all[warp];
   const int a = ta * 32 + lane;
   const int bb = tb * 32 + warp * 4;
   c32 acc[4][NB];
@@ -184,40 +203,54 @@ k_spread(const c32* __restrict__ c, long long c_stride, int nslices, int os, int
     for (int j = 0; j < NB; ++j) acc[i][j] = mk(0.f, 0.f);
   // this warp's list: the samples whose window touches its 4-row band
   const int beg = __ldg(tile_ptr + tile * 8 + warp), end = __ldg(tile_ptr + tile * 8 + warp + 1);
-  // one-sample-ahead software pipeline: the index chain tile_idx -> ab -> weights /
-  // values of sample q+1 is in flight while sample q accumulates
-  int m_n = 0;
-  int2 s_n = make_int2(0, 0);
-  if (beg < end) {
-    m_n = __ldg(tile_idx + beg);
-    s_n = __ldg(ab + m_n);
-  }
-  for (int q = beg; q < end; ++q) {
-    const int m = m_n;
-    const int2 s = s_n;
-    if (q + 1 < end) {
-      m_n = __ldg(tile_idx + q + 1);
-      s_n = __ldg(ab + m_n);
+  // registers of the chunk in flight (lane l: sample base + l)
+  int2 r_ab = make_int2(0, 0);
+  float r_w[2 * W];
+  c32 r_cv[NB];
+  auto fetch = [&](int base) {
+    const int q = base + lane;
+    if (q < end) {
+      const int m = __ldg(tile_idx + q);
+      r_ab = __ldg(ab + m);
+      const float* wr = wts + (long long)m * (2 * W);
+#pragma unroll
+      for (int k = 0; k < 2 * W; ++k) r_w[k] = __ldg(wr + k);
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        r_cv[j] = (z0 + j < nslices) ? __ldg(c + (long long)(z0 + j) * c_stride + m) : mk(0.f, 0.f);
     }
-    int db = bb - s.y;
-    if (db < 0) db += os;
-    if (db >= W && db <= os - 4) continue;  // none of this warp's rows (warp-uniform)
-    int da = a - s.x;
-    if (da < 0) da += os;
-    const float* wr = wts + (long long)m * (2 * W);
-    const float wx = da < W ? __ldg(wr + da) : 0.f;
-    c32 cv[NB];
+  };
+  if (beg < end) fetch(beg);
+  for (int base = beg; base < end; base += 32) {
+    const int cnt = min(32, end - base);
+    __syncwarp();  // the previous chunk is consumed
+    st.ab[lane] = r_ab;
 #pragma unroll
-    for (int j = 0; j < NB; ++j)
-      cv[j] = (z0 + j < nslices) ? __ldg(c + (long long)(z0 + j) * c_stride + m) : mk(0.f, 0.f);
+    for (int k = 0; k < 2 * W; ++k) st.w[lane][k] = r_w[k];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      int d = db + i;
-      if (d >= os) d -= os;
-      if (d < W) {
-        const float w = wx * __ldg(wr + W + d);
+    for (int j = 0; j < NB; ++j) st.cv[lane][j] = r_cv[j];
+    __syncwarp();
+    if (base + 32 < end) fetch(base + 32);
+    for (int q = 0; q < cnt; ++q) {
+      const int2 s = st.ab[q];
+      int db = bb - s.y;
+      if (db < 0) db += os;
+      if (db >= W && db <= os - 4) continue;  // none of this warp's rows (warp-uniform)
+      int da = a - s.x;
+      if (da < 0) da += os;
+      const float wx = da < W ? st.w[q][da] : 0.f;
+      c32 cv[NB];
 #pragma unroll
-        for (int j = 0; j < NB; ++j) acc[i][j] = pfma(cv[j], mk(w, w), acc[i][j]);
+      for (int j = 0; j < NB; ++j) cv[j] = st.cv[q][j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int d = db + i;
+        if (d >= os) d -= os;
+        if (d < W) {
+          const float w = wx * st.w[q][W + d];
+#pragma unroll
+          for (int j = 0; j < NB; ++j) acc[i][j] = pfma(cv[j], mk(w, w), acc[i][j]);
+        }
       }
     }
   }

@@ -76,68 +76,116 @@ int launch_resample(const float* in, float* out, long long outer, int n_src, int
 }
 
 // ---------------------------------------------------------------- fused 3-axis
-// All three axes in one pass (multires.py:186-191): a CTA owns a 32 (x) x 128 (y)
-// target tile and walks target planes t.  Per plane it z-interpolates the tile's
-// source window straight from global memory (the band's planes are L2-resident
-// across neighbouring t) into shared memory, interpolates x into a second
-// buffer, then y on the way out -- one read of the source window and one write
-// of the target: ~4.5 B per fine voxel at ratio 2, instead of three full
-// intermediate volumes.
-constexpr int UP_TX = 128, UP_TY = 32;      // target tile (y contiguous, x rows)
-constexpr int UP_CMAX = UP_TX + 8, UP_RMAX = UP_TY + 8;  // source window at ratio <= 1
+// All three axes in one pass (multires.py:186-191).  A CTA owns a 32 (x) x 128
+// (y) target tile and walks its run of target planes t.  The tile's source
+// window (nr x nc cells per coarse plane) of every coarse plane it needs is
+// copied into a shared-memory ring (cp.async, one copy per cell) exactly once;
+// the plane the next target needs is in flight while the current target is
+// interpolated: z from the ring into t1, x into t2, y on the way out.  HBM
+// traffic: the source read once (plus the window halo) and the target written
+// once -- ~4.5 B per fine voxel at ratio 2.  Upsampling only: consecutive target
+// planes advance the z band by at most one coarse plane, so kz + 1 ring slots
+// suffice.
+constexpr int UP_TX = 128, UP_TY = 32;  // target tile (y contiguous, x rows)
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 __global__ void __launch_bounds__(256)
 k_upsample3(const float* __restrict__ src, float* __restrict__ out, int hs, int ws, int t_begin,
             int nzt, int zper, int ht, int wt, const int* __restrict__ sz,
             const float* __restrict__ wz, int kz, const int* __restrict__ sx,
             const float* __restrict__ wx, int kx, const int* __restrict__ sy,
-            const float* __restrict__ wy, int ky) {
-  __shared__ float t1[UP_RMAX * UP_CMAX];  // z-interpolated source window
-  __shared__ float t2[UP_TY * UP_CMAX];    // then x-interpolated
+            const float* __restrict__ wy, int ky, int nrm, int ncm) {
+  extern __shared__ __align__(16) float up_sm[];
+  const int ring_n = kz + 1;
+  const int pw = nrm * ncm;                 // words per ring plane
+  float* ring = up_sm;                      // [ring_n][nrm][ncm]
+  float* t1 = ring + ring_n * pw;           // z-interpolated window [nrm][ncm]
+  float* t2 = t1 + pw;                      // then x-interpolated [UP_TY][ncm]
+  float* wxs = t2 + UP_TY * ncm;            // x taps of the tile rows [UP_TY][8]
+  int* rss = reinterpret_cast<int*>(wxs + UP_TY * 8);  // their window rows [UP_TY]
   const int j0 = blockIdx.x * UP_TX, i0 = blockIdx.y * UP_TY;
   const int jn = min(UP_TX, wt - j0), in_ = min(UP_TY, ht - i0);
   const int r0 = __ldg(sx + i0), c0 = __ldg(sy + j0);
   const int nr = __ldg(sx + i0 + in_ - 1) + kx - r0;
   const int nc = __ldg(sy + j0 + jn - 1) + ky - c0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < UP_TY) {
+    const int i = threadIdx.x;
+    rss[i] = i < in_ ? __ldg(sx + i0 + i) - r0 : 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wxs[i * 8 + k] = (i < in_ && k < kx) ? __ldg(wx + (i0 + i) * kx + k) : 0.f;
+  }
   // y taps of this thread's target column (fixed for the whole CTA)
   const int j = threadIdx.x % UP_TX, ib = threadIdx.x / UP_TX;
   float wyr[8];
   int ys = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) wyr[k] = 0.f;
   if (j < jn) {
     ys = __ldg(sy + j0 + j) - c0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) wyr[k] = k < ky ? __ldg(wy + (j0 + j) * ky + k) : 0.f;
   }
   const long long plane = (long long)hs * ws;
+  auto load_plane = [&](int s) {  // coarse plane s -> its ring slot
+    const float* sp = src + (long long)s * plane + (long long)r0 * ws + c0;
+    float* dst = ring + (s % ring_n) * pw;
+    for (int r = warp; r < nr; r += 8)
+      for (int c = lane; c < nc; c += 32) cp_async4(dst + r * ncm + c, sp + (long long)r * ws + c);
+  };
   const int z_lo = blockIdx.z * zper, z_hi = min(nzt, z_lo + zper);
+  if (z_lo >= z_hi) return;
+  int hi = __ldg(sz + t_begin + z_lo);
+  for (int k = 0; k < kz; ++k) load_plane(hi++);
+  cp_async_commit();
   for (int tz = z_lo; tz < z_hi; ++tz) {
     const int t = t_begin + tz;
-    const float* sp = src + (long long)__ldg(sz + t) * plane + (long long)r0 * ws + c0;
-    const float* wzt = wz + (long long)t * kz;
-    for (int e = threadIdx.x; e < nr * UP_CMAX; e += 256) {
-      const int r = e / UP_CMAX, c = e - r * UP_CMAX;
-      if (c < nc) {
-        float a = 0.f;
-        for (int k = 0; k < kz; ++k) a = fmaf(__ldg(wzt + k), __ldg(sp + k * plane + (long long)r * ws + c), a);
-        t1[e] = a;
-      }
-    }
+    const int s_lo = __ldg(sz + t);
+    // the coarse plane the next target adds (at most one when upsampling)
+    if (tz + 1 < z_hi && __ldg(sz + t + 1) + kz > hi) load_plane(hi++);
+    cp_async_commit();
+    cp_async_wait<1>();  // everything but the plane just issued
     __syncthreads();
-    for (int e = threadIdx.x; e < in_ * UP_CMAX; e += 256) {
-      const int i = e / UP_CMAX, c = e - i * UP_CMAX;
-      if (c < nc) {
-        const int rs = __ldg(sx + i0 + i) - r0;
-        const float* wxi = wx + (long long)(i0 + i) * kx;
+    const float* wzt = wz + (long long)t * kz;
+    float wzr[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wzr[k] = k < kz ? __ldg(wzt + k) : 0.f;
+    for (int r = warp; r < nr; r += 8)
+      for (int c = lane; c < nc; c += 32) {
         float a = 0.f;
-        for (int k = 0; k < kx; ++k) a = fmaf(__ldg(wxi + k), t1[(rs + k) * UP_CMAX + c], a);
-        t2[e] = a;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < kz) a = fmaf(wzr[k], ring[((s_lo + k) % ring_n) * pw + r * ncm + c], a);
+        t1[r * ncm + c] = a;
+      }
+    __syncthreads();
+    for (int i = warp; i < in_; i += 8) {
+      const float* src_r = t1 + rss[i] * ncm;
+      const float* w8 = wxs + i * 8;
+      for (int c = lane; c < nc; c += 32) {
+        float a = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < kx) a = fmaf(w8[k], src_r[k * ncm + c], a);
+        t2[i * ncm + c] = a;
       }
     }
     __syncthreads();
     if (j < jn) {
       float* op = out + ((long long)tz * ht + i0) * wt + j0 + j;
       for (int i = ib; i < in_; i += 256 / UP_TX) {
-        const float* row = t2 + i * UP_CMAX + ys;
+        const float* row = t2 + i * ncm + ys;
         float a = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
@@ -145,26 +193,34 @@ k_upsample3(const float* __restrict__ src, float* __restrict__ out, int hs, int 
         op[(long long)i * wt] = a;
       }
     }
-    __syncthreads();  // t1/t2 are rewritten for the next plane
   }
+  cp_async_wait<0>();
 }
 
 int upsample3(const float* src, int zs, int hs, int ws, float* out, int t_begin, int nzt, int ht,
               int wt, const int* sz, const float* wz, int kz, const int* sx, const float* wx, int kx,
-              const int* sy, const float* wy, int ky, cudaStream_t st) {
+              const int* sy, const float* wy, int ky, int nrm, int ncm, cudaStream_t st) {
   if ((long long)nzt * ht * wt == 0) return TF_OK;
   if (kz < 1 || kz > 8 || kx < 1 || kx > 8 || ky < 1 || ky > 8)
     return fail_arg("upsample bands must have 1..8 taps (got %d, %d, %d)", kz, kx, ky);
   if (hs > ht || ws > wt) return fail_arg("upsample3 cannot reduce the grid");
+  if (nrm < 1 || ncm < 1 || nrm > UP_TY + 8 || ncm > UP_TX + 8)
+    return fail_arg("upsample3 window %d x %d out of range", nrm, ncm);
   (void)zs;
+  const size_t smem = sizeof(float) * ((size_t)(kz + 3) * nrm * ncm + UP_TY * ncm + UP_TY * 9);
+  TF_TRY(prep_kernel(k_upsample3, smem));
+  int per_sm = 0;
+  TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_upsample3, 256, smem),
+                    "occupancy"));
   const int gx = (wt + UP_TX - 1) / UP_TX, gy = (ht + UP_TY - 1) / UP_TY;
-  // enough CTAs for ~4 waves of 148 SMs; each walks a run of target planes
+  // split the target planes only when the tiles alone cannot fill ~2 waves
   const long long tiles = (long long)gx * gy;
-  const int zch = (int)std::max<long long>(1, std::min<long long>(nzt, (4 * 148 * 5 + tiles - 1) / tiles));
+  const long long want = 2LL * std::max(1, per_sm) * num_sms();
+  const int zch = (int)std::max<long long>(1, std::min<long long>(nzt, (want + tiles - 1) / tiles));
   const int zper = (nzt + zch - 1) / zch;
   const dim3 g(gx, gy, (nzt + zper - 1) / zper);
-  k_upsample3<<<g, 256, 0, st>>>(src, out, hs, ws, t_begin, nzt, zper, ht, wt, sz, wz, kz, sx, wx,
-                                 kx, sy, wy, ky);
+  k_upsample3<<<g, 256, smem, st>>>(src, out, hs, ws, t_begin, nzt, zper, ht, wt, sz, wz, kz, sx,
+                                    wx, kx, sy, wy, ky, nrm, ncm);
   return check_launch("k_upsample3");
 }
 

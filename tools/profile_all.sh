@@ -7,10 +7,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-mbir > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_rows|k_cols_conv' -s 6 -c 3 \
   -o gpurun_out/prof_toeplitz_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-mbir > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_prior|k_energy' -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_prior|k_energy' -c 4 \
   -o gpurun_out/prof_solver_$TAG -f python tools/solver_probe.py > /dev/null 2>&1
 PROBE_SLICES=8 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:'k_spread|k_nufft|k_detector|k_resample|k_plan' -c 12 \
+  -k regex:'k_spread|k_nufft|k_detector|k_resample|k_upsample|k_plan' -c 14 \
   -o gpurun_out/prof_onetime_$TAG -f python tools/nufft_probe.py > /dev/null 2>&1
 timeout 300 python tools/nufft_probe.py > gpurun_out/nufft_probe_$TAG.json 2>&1
 timeout 300 python tools/solver_probe.py > gpurun_out/solver_probe_$TAG.json 2>&1
