@@ -100,12 +100,17 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// KT > 0: every axis has KT taps (compile time: 6 for the Lanczos-3 doubling of the
+// schedule); KT == 0: per-axis tap counts <= 8 at run time
+template <int KT>
 __global__ void __launch_bounds__(256)
 k_upsample3(const float* __restrict__ src, float* __restrict__ out, int hs, int ws, int t_begin,
             int nzt, int zper, int ht, int wt, const int* __restrict__ sz,
-            const float* __restrict__ wz, int kz, const int* __restrict__ sx,
-            const float* __restrict__ wx, int kx, const int* __restrict__ sy,
-            const float* __restrict__ wy, int ky, int nrm, int ncm) {
+            const float* __restrict__ wz, int kz_rt, const int* __restrict__ sx,
+            const float* __restrict__ wx, int kx_rt, const int* __restrict__ sy,
+            const float* __restrict__ wy, int ky_rt, int nrm, int ncm) {
+  constexpr int KM = KT > 0 ? KT : 8;  // unrolled tap loops
+  const int kz = KT > 0 ? KT : kz_rt, kx = KT > 0 ? KT : kx_rt, ky = KT > 0 ? KT : ky_rt;
   extern __shared__ __align__(16) float up_sm[];
   const int ring_n = kz + 1;
   const int pw = nrm * ncm;                 // words per ring plane
@@ -128,14 +133,14 @@ k_upsample3(const float* __restrict__ src, float* __restrict__ out, int hs, int 
   }
   // y taps of this thread's target column (fixed for the whole CTA)
   const int j = threadIdx.x % UP_TX, ib = threadIdx.x / UP_TX;
-  float wyr[8];
+  float wyr[KM];
   int ys = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) wyr[k] = 0.f;
+  for (int k = 0; k < KM; ++k) wyr[k] = 0.f;
   if (j < jn) {
     ys = __ldg(sy + j0 + j) - c0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) wyr[k] = k < ky ? __ldg(wy + (j0 + j) * ky + k) : 0.f;
+    for (int k = 0; k < KM; ++k) wyr[k] = k < ky ? __ldg(wy + (j0 + j) * ky + k) : 0.f;
   }
   const long long plane = (long long)hs * ws;
   auto load_plane = [&](int s) {  // coarse plane s -> its ring slot
@@ -158,25 +163,34 @@ k_upsample3(const float* __restrict__ src, float* __restrict__ out, int hs, int 
     cp_async_wait<1>();  // everything but the plane just issued
     __syncthreads();
     const float* wzt = wz + (long long)t * kz;
-    float wzr[8];
+    float wzr[KM];
+    const float* pl[KM];  // ring slots of the band's planes (no modulo in the cell loop)
+    int slot = s_lo % ring_n;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) wzr[k] = k < kz ? __ldg(wzt + k) : 0.f;
+    for (int k = 0; k < KM; ++k) {
+      wzr[k] = k < kz ? __ldg(wzt + k) : 0.f;
+      pl[k] = ring + slot * pw;
+      slot = slot + 1 == ring_n ? 0 : slot + 1;
+    }
     for (int r = warp; r < nr; r += 8)
       for (int c = lane; c < nc; c += 32) {
+        const int off = r * ncm + c;
         float a = 0.f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (k < kz) a = fmaf(wzr[k], ring[((s_lo + k) % ring_n) * pw + r * ncm + c], a);
-        t1[r * ncm + c] = a;
+        for (int k = 0; k < KM; ++k)
+          if (k < kz) a = fmaf(wzr[k], pl[k][off], a);
+        t1[off] = a;
       }
     __syncthreads();
     for (int i = warp; i < in_; i += 8) {
       const float* src_r = t1 + rss[i] * ncm;
-      const float* w8 = wxs + i * 8;
+      float w8[KM];
+#pragma unroll
+      for (int k = 0; k < KM; ++k) w8[k] = wxs[i * 8 + k];
       for (int c = lane; c < nc; c += 32) {
         float a = 0.f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < KM; ++k)
           if (k < kx) a = fmaf(w8[k], src_r[k * ncm + c], a);
         t2[i * ncm + c] = a;
       }
@@ -188,7 +202,7 @@ k_upsample3(const float* __restrict__ src, float* __restrict__ out, int hs, int 
         const float* row = t2 + i * ncm + ys;
         float a = 0.f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < KM; ++k)
           if (k < ky) a = fmaf(wyr[k], row[k], a);
         op[(long long)i * wt] = a;
       }
@@ -208,9 +222,10 @@ int upsample3(const float* src, int zs, int hs, int ws, float* out, int t_begin,
     return fail_arg("upsample3 window %d x %d out of range", nrm, ncm);
   (void)zs;
   const size_t smem = sizeof(float) * ((size_t)(kz + 3) * nrm * ncm + UP_TY * ncm + UP_TY * 9);
-  TF_TRY(prep_kernel(k_upsample3, smem));
+  auto kern = (kz == 6 && kx == 6 && ky == 6) ? k_upsample3<6> : k_upsample3<0>;
+  TF_TRY(prep_kernel(kern, smem));
   int per_sm = 0;
-  TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_upsample3, 256, smem),
+  TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem),
                     "occupancy"));
   const int gx = (wt + UP_TX - 1) / UP_TX, gy = (ht + UP_TY - 1) / UP_TY;
   // split the target planes only when the tiles alone cannot fill ~2 waves
@@ -219,8 +234,8 @@ int upsample3(const float* src, int zs, int hs, int ws, float* out, int t_begin,
   const int zch = (int)std::max<long long>(1, std::min<long long>(nzt, (want + tiles - 1) / tiles));
   const int zper = (nzt + zch - 1) / zch;
   const dim3 g(gx, gy, (nzt + zper - 1) / zper);
-  k_upsample3<<<g, 256, smem, st>>>(src, out, hs, ws, t_begin, nzt, zper, ht, wt, sz, wz, kz, sx,
-                                    wx, kx, sy, wy, ky, nrm, ncm);
+  kern<<<g, 256, smem, st>>>(src, out, hs, ws, t_begin, nzt, zper, ht, wt, sz, wz, kz, sx, wx, kx,
+                             sy, wy, ky, nrm, ncm);
   return check_launch("k_upsample3");
 }
 
