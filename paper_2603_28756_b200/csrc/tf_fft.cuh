@@ -57,12 +57,29 @@ __device__ __forceinline__ c32 tw_w(int k) {
 constexpr float kH = 0.70710678118654752440f;  // 1/sqrt 2
 
 // ---------------------------------------------------- FMA-folded codelet
-// cos(2 pi q / 16); W_16^q = (cos16(q), -cos16(q - 4)).  q is a constant after
-// unrolling, so the lookup folds to an immediate.
-__device__ __forceinline__ float cos16(int q) {
-  constexpr float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;
-  const float c[16] = {1.f, c1, kH, s1, 0.f, -s1, -kH, -c1, -1.f, -c1, -kH, -s1, 0.f, s1, kH, c1};
-  return c[q & 15];
+// cos(2 pi q / 64); W_n^q = (cos64(64q/n), -cos64(64q/n - 16)) for n | 64.  q is a
+// constant after unrolling, so the lookup folds to an immediate.  (The 16ths are
+// the same fp32 values the radix-16 codelets always used.)
+__device__ __forceinline__ float cos64(int q) {
+  const float c[64] = {
+      1.f, 0.9951847195625305f, 0.9807852506637573f, 0.9569403529167175f,
+      0.9238795042037964f, 0.8819212913513184f, 0.8314695954322815f, 0.7730104327201843f,
+      0.7071067690849304f, 0.6343932747840881f, 0.5555702447891235f, 0.4713967442512512f,
+      0.3826834261417389f, 0.290284663438797f, 0.19509032368659973f, 0.0980171412229538f,
+      0.f, -0.0980171412229538f, -0.19509032368659973f, -0.290284663438797f,
+      -0.3826834261417389f, -0.4713967442512512f, -0.5555702447891235f, -0.6343932747840881f,
+      -0.7071067690849304f, -0.7730104327201843f, -0.8314695954322815f, -0.8819212913513184f,
+      -0.9238795042037964f, -0.9569403529167175f, -0.9807852506637573f, -0.9951847195625305f,
+      -1.f, -0.9951847195625305f, -0.9807852506637573f, -0.9569403529167175f,
+      -0.9238795042037964f, -0.8819212913513184f, -0.8314695954322815f, -0.7730104327201843f,
+      -0.7071067690849304f, -0.6343932747840881f, -0.5555702447891235f, -0.4713967442512512f,
+      -0.3826834261417389f, -0.290284663438797f, -0.19509032368659973f, -0.0980171412229538f,
+      0.f, 0.0980171412229538f, 0.19509032368659973f, 0.290284663438797f,
+      0.3826834261417389f, 0.4713967442512512f, 0.5555702447891235f, 0.6343932747840881f,
+      0.7071067690849304f, 0.7730104327201843f, 0.8314695954322815f, 0.8819212913513184f,
+      0.9238795042037964f, 0.9569403529167175f, 0.9807852506637573f, 0.9951847195625305f,
+  };
+  return c[q & 63];
 }
 
 // e + o t (forward) or e + o conj(t) (INV): two FFMA2
@@ -95,7 +112,7 @@ __device__ __forceinline__ void fold_level(const c32 (&a)[R], c32 (&b)[R], const
     ws = pw[LR - LV];
 #pragma unroll
     for (int qp = 1; qp < nq; ++qp)
-      tq[qp] = cmul(ws, mk(cos16(qp * 16 / n), -cos16(qp * 16 / n - 4)));
+      tq[qp] = cmul(ws, mk(cos64(qp * 64 / n), -cos64(qp * 64 / n - 16)));
   }
 #pragma unroll
   for (int r0 = 0; r0 < s; ++r0) {
@@ -117,7 +134,7 @@ __device__ __forceinline__ void fold_level(const c32 (&a)[R], c32 (&b)[R], const
         } else {
           c32 t = qp == 0 ? ws
                   : TW    ? tq[qp]
-                          : mk(cos16(qp * 16 / n), -cos16(qp * 16 / n - 4));
+                          : mk(cos64(qp * 64 / n), -cos64(qp * 64 / n - 16));
           if (quarter) t = mk(t.y, -t.x);  // -i t
           const c32 z = cfma<INV>(e, o, t);
           b[pos0] = z;

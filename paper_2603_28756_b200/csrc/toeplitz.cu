@@ -550,6 +550,151 @@ k_cols_conv_pp(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__
   }
 }
 
+// K2 for M = 2048 / 4096 on two radix-64-sized passes: E = 64 elements per thread,
+// TT = M/64 threads per column transform (one or two warps), G = 4 independent
+// groups per CTA, one CTA per SM.  Against k_cols_conv_pp (E = 16, three passes)
+// this halves the shared-memory exchanges per (column, slice) item -- one
+// exchange per transform instead of two, 2 x 32 KB stored and loaded instead of
+// 4 x 32 KB -- which, with the FP32 pipe, bound the column pass (an exchange-only
+// variant of k_cols_conv_pp ran 1.23 ms of its 1.99 ms; profiles/r02).
+// * The CTA walks columns c = blockIdx.x + k gridDim.x; its four groups split the
+//   column's slices (group g: z = g, g+4, ...).  64 complex elements per thread
+//   leave no registers for the PSF, so the column's PSF (12 B per frequency) is
+//   bulk-copied into shared memory once per column (CTA barrier at each column
+//   change; the copy is waited for only at the PSF product).  Reading it through
+//   L1 instead doubled the kernel time (the 48 KB column does not stay in L1 next
+//   to ~180 KB of shared memory).
+// * Each group runs its own pipeline over named barriers of its TT threads.  The
+//   next item's 4-D TMA gather lands in the group's exchange buffer as soon as the
+//   second exchange has been read (`empty` mbarrier), i.e. during the last pass
+//   and the stores, so no separate input stage is needed.
+// * The pass-1 twiddles depend only on the thread (k = t): computed once.
+// * Exchange padding: word w at w + w/TT (pass-0 radix == TT, so a thread's
+//   pass-0 outputs and the canonical reads both hit distinct bank pairs).
+template <int M, bool FLIP>
+__global__ void __launch_bounds__(4 * (M / 64), 1)
+k_cols_conv64(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ PQ,
+              const float* __restrict__ Bi, int ncols, int nrb, int nslices, int boxr,
+              c32* __restrict__ T) {
+  constexpr int E = 64, TT = M / E, G = 4;
+  constexpr int H = M / 2 + 1;
+  constexpr int XW = M + M / TT;  // padded exchange words per group
+  using S = FftShape<M, E>;
+  static_assert(S::NP == 2 && (1 << S::LFIRST) == TT, "two passes, pass-0 radix == TT");
+  constexpr int R0 = TT, ST0 = E / R0;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int g = threadIdx.x / TT, t = threadIdx.x - g * TT;
+  c32* pq_s = reinterpret_cast<c32*>(smem_raw);                  // [M]
+  float* bi_s = reinterpret_cast<float*>(pq_s + M);                // [M]
+  c32* xb = reinterpret_cast<c32*>(bi_s + M) + g * XW;             // [G][XW]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<c32*>(bi_s + M) + G * XW);
+  uint64_t* full = bars + 2 * g;
+  uint64_t* empty = full + 1;
+  uint64_t* psf_full = bars + 2 * G;
+  const int bar_id = 1 + g;
+  if (threadIdx.x == 0) mbar_init(psf_full, 1);
+  if (t == 0) {
+    mbar_init(full, 1);
+    mbar_init(empty, TT);
+  }
+  if (threadIdx.x == 0) fence_mbar_init();
+  __syncthreads();
+  if ((int)blockIdx.x >= ncols) return;
+  const bool active = g < nslices;
+  const int my_cols = (ncols - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int nz_g = active ? (nslices - g + G - 1) / G : 0;
+  const int nitems = my_cols * nz_g;
+  const int nbox = (nrb + boxr - 1) / boxr;
+  const uint32_t box_bytes = (uint32_t)boxr * RB * sizeof(c32);
+  const int col_len = nrb * RB;
+  int p_col = blockIdx.x, p_z = g, issued = 0;
+  auto issue = [&]() {
+    mbar_expect_tx(full, nbox * box_bytes);
+    for (int q = 0; q < nbox; ++q)
+      tma_load_4d(xb + q * boxr * RB, &tmap, 0, p_col, q * boxr, p_z, full);
+    ++issued;
+    p_z += G;
+    if (p_z >= nslices) {
+      p_z = g;
+      p_col += gridDim.x;
+    }
+  };
+  if (t == 0 && nitems > 0) {
+    tma_prefetch_desc(&tmap);
+    issue();
+  }
+  PassTw<M, E, 1> tw;
+  tw.from_table(t);
+  const long long m_stride = (long long)(TT / RB) * H * RB;
+  const long long slice_stride = (long long)nrb * H * RB;
+  const long long t_off = (long long)(t >> 2) * H * RB + (t & 3);
+  auto exchange = [&](c32 (&v)[1][E]) {
+#pragma unroll
+    for (int i = 0; i < ST0; ++i)
+#pragma unroll
+      for (int r = 0; r < R0; ++r) xb[(t + i * TT) * (R0 + 1) + r] = v[0][i + r * ST0];
+    named_bar_sync(bar_id, TT);
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[0][m] = xb[t + (TT + 1) * m];
+  };
+  int item = 0;
+  for (int k = 0; k < my_cols; ++k) {
+    const int c = blockIdx.x + k * gridDim.x;
+    __syncthreads();  // every group is done with the previous column's PSF
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(psf_full, M * (uint32_t)(sizeof(c32) + (FLIP ? sizeof(float) : 0)));
+      bulk_g2s(pq_s, PQ + (long long)c * M, M * sizeof(c32), psf_full);
+      if constexpr (FLIP) bulk_g2s(bi_s, Bi + (long long)c * M, M * sizeof(float), psf_full);
+      if (k + 1 < my_cols) {
+        bulk_prefetch_l2(PQ + (long long)(c + gridDim.x) * M, M * sizeof(c32));
+        if constexpr (FLIP) bulk_prefetch_l2(Bi + (long long)(c + gridDim.x) * M, M * sizeof(float));
+      }
+    }
+    bool psf_ready = false;
+    for (int z = g; active && z < nslices; z += G, ++item) {
+      mbar_wait(full, (uint32_t)(item & 1));
+      c32 v[1][E];
+#pragma unroll
+      for (int m = 0; m < E / 2; ++m) {
+        const int j = t + TT * m;
+        v[0][m] = j < col_len ? xb[j] : mk(0.f, 0.f);
+      }
+      fft_pass<M, E, 0, false, true, false, 1>(v, (const PassTw<M, E, 0>*)nullptr);
+      named_bar_sync(bar_id, TT);  // the input (in xb) has been read by the whole group
+      exchange(v);
+      fft_pass<M, E, 1, false, false, false, 1>(v, &tw);
+      if (!psf_ready) {
+        mbar_wait(psf_full, (uint32_t)(k & 1));
+        psf_ready = true;
+      }
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        const c32 pq = pq_s[t + TT * m];
+        if constexpr (FLIP) {
+          const float bi = bi_s[t + TT * m];
+          v[0][m] = pfma(mk(v[0][m].y, v[0][m].x), mk(bi, bi), pmul(v[0][m], pq));
+        } else {
+          v[0][m] = pmul(v[0][m], pq);
+        }
+      }
+      fft_pass<M, E, 0, true, false, false, 1>(v, (const PassTw<M, E, 0>*)nullptr);
+      named_bar_sync(bar_id, TT);  // the first exchange has been read
+      exchange(v);
+      mbar_arrive(empty);
+      if (t == 0 && issued < nitems) {
+        mbar_wait(empty, (uint32_t)(item & 1));
+        issue();
+      }
+      fft_pass<M, E, 1, true, false, true, 1>(v, &tw);
+      c32* dst = T + z * slice_stride + (long long)c * RB + t_off;
+#pragma unroll
+      for (int m = 0; m < E / 2; ++m) {
+        if (t + TT * m < col_len) dst[m * m_stride] = v[0][m];
+      }
+    }
+  }
+}
+
 // forward-only column FFT (PSF spectra): S[z][c][kx] = FFT_ix(column c of T)
 template <int M, int E, int G>
 __global__ void __launch_bounds__(G*(M / E))
@@ -836,6 +981,27 @@ int launch_cols_conv_pp_t(c32* T, const c32* PQ, const float* Bi, int col_len,
 }
 
 template <int M, bool FLIP>
+int launch_cols_conv64_t(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
+                         cudaStream_t st) {
+  constexpr int TT = M / 64, G = 4;
+  const int ncols = M / 2 + 1;
+  const int nrb = nrb_of(col_len);
+  const int boxr = std::min(nrb, 256);
+  CUtensorMap map;
+  TF_TRY(encode_tmap(&map, T, M, nrb, nslices, boxr));
+  const size_t smem = (sizeof(c32) + sizeof(float)) * M + sizeof(c32) * G * (size_t)(M + M / TT) +
+                      (2 * G + 1) * sizeof(uint64_t);
+  auto kern = k_cols_conv64<M, FLIP>;
+  TF_TRY(prep_kernel(kern, smem));
+  const int grid = std::max(1, std::min(ncols, num_sms()));
+  KernelTimer tm;
+  timer_begin(tm, 1, st);
+  kern<<<grid, G * TT, smem, st>>>(map, PQ, Bi, ncols, nrb, (int)nslices, boxr, T);
+  timer_end(tm);
+  return check_launch("k_cols_conv64");
+}
+
+template <int M, bool FLIP>
 int launch_cols_conv_t(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
                        cudaStream_t st) {
   constexpr int E = eper<M>(), G = cols_g<M>();
@@ -859,6 +1025,13 @@ template <int M>
 int launch_cols_conv(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
                      bool flip, cudaStream_t st) {
   if (2 * col_len > M) return fail_arg("k_cols_conv: column length %d exceeds M/2", col_len);
+#ifndef TF_K2_E64
+#define TF_K2_E64 1
+#endif
+  if constexpr (TF_K2_E64 && (M == 2048 || M == 4096)) {
+    return flip ? launch_cols_conv64_t<M, true>(T, PQ, Bi, col_len, nslices, st)
+                : launch_cols_conv64_t<M, false>(T, PQ, Bi, col_len, nslices, st);
+  }
   if constexpr (M >= 1024 && M <= 4096) {
     return flip ? launch_cols_conv_pp_t<M, true>(T, PQ, Bi, col_len, nslices, st)
                 : launch_cols_conv_pp_t<M, false>(T, PQ, Bi, col_len, nslices, st);
