@@ -2,7 +2,7 @@
 //
 // A length-M transform is run by a *group* of T = M/E threads; thread t keeps
 // the E elements {t + T*m : m < E} in registers ("canonical layout").  Each
-// pass applies radix-R butterflies (R | E, R <= 16) to register-resident data;
+// pass applies radix-R butterflies (R | E, R <= 64) to register-resident data;
 // between passes the group exchanges through a padded shared-memory buffer
 // (word i lives at i + i/16, which keeps every exchange at the 2-wavefront
 // minimum for 8-byte elements).  The first radix may be smaller than E, all
@@ -159,74 +159,6 @@ __device__ __forceinline__ void fold_levels(c32 (&a)[R], const c32* pw) {
 template <int R, bool INV, bool ZIN, bool HOUT, bool TW>
 __device__ __forceinline__ void dft_fold(c32 (&u)[R], const c32* pw) {
   fold_levels<R, 1, INV, ZIN, HOUT, TW>(u, pw);
-}
-
-// ---- twiddled fold with the step twiddles read from a per-thread table
-// Level LV (n = 2^LV) of a twiddled radix-R fold uses nq(LV) = max(1, n/4) values
-// w^s W_n^{q'} (q' < nq, s = R/n); tw_tab_words<R>() of them per thread, level LV
-// at word offset tw_tab_off(LV), entry e of thread t at tab[e * TSTRIDE] (the
-// caller passes tab = base + t, so a warp reads consecutive words).
-__host__ __device__ constexpr int tw_nq(int LV) { return LV >= 2 ? (1 << LV) / 4 : 1; }
-__host__ __device__ constexpr int tw_tab_off(int LV) { return LV <= 1 ? 0 : tw_tab_off(LV - 1) + tw_nq(LV - 1); }
-template <int R>
-__host__ __device__ constexpr int tw_tab_words() { return tw_tab_off(ilog2(R) + 1); }
-
-template <int R, int LV, bool INV, bool HOUT, int TSTRIDE>
-__device__ __forceinline__ void fold_level_tab(const c32 (&a)[R], c32 (&b)[R], const c32* tab) {
-  constexpr int LR = ilog2(R);
-  constexpr int n = 1 << LV, s = R >> LV, h = n >> 1, nq = tw_nq(LV);
-  constexpr bool last = LV == LR;
-  c32 tq[nq];
-#pragma unroll
-  for (int qp = 0; qp < nq; ++qp) tq[qp] = tab[(tw_tab_off(LV) + qp) * TSTRIDE];
-#pragma unroll
-  for (int r0 = 0; r0 < s; ++r0) {
-#pragma unroll
-    for (int q = 0; q < h; ++q) {
-      const int pos0 = r0 + s * q, pos1 = pos0 + R / 2;
-      const c32 e = a[r0 + 2 * s * q];
-      const c32 o = a[r0 + s + 2 * s * q];
-      c32 t = tq[q % nq];
-      if (n >= 4 && q >= nq) t = mk(t.y, -t.x);  // -i t
-      const c32 z = cfma<INV>(e, o, t);
-      b[pos0] = z;
-      if constexpr (!(HOUT && last)) b[pos1] = twice_minus(e, z);
-    }
-  }
-}
-
-template <int R, int LV, bool INV, bool HOUT, int TSTRIDE>
-__device__ __forceinline__ void fold_levels_tab(c32 (&a)[R], const c32* tab) {
-  if constexpr (LV <= ilog2(R)) {
-    c32 b[R];
-    fold_level_tab<R, LV, INV, HOUT, TSTRIDE>(a, b, tab);
-    fold_levels_tab<R, LV + 1, INV, HOUT, TSTRIDE>(b, tab);
-#pragma unroll
-    for (int r = 0; r < R; ++r) a[r] = b[r];
-  }
-}
-
-// X[q] = sum_r u_r w^r W_R^{rq} (conjugated for INV) with the step twiddles of the
-// thread's w from `tab` (see tw_tab_fill)
-template <int R, bool INV, bool HOUT, int TSTRIDE>
-__device__ __forceinline__ void dft_fold_tab(c32 (&u)[R], const c32* tab) {
-  fold_levels_tab<R, 1, INV, HOUT, TSTRIDE>(u, tab);
-}
-
-// entries of the table for the twiddle w = e^{-2 pi i k / L} (fp64, rounded once):
-// level LV, q' -> e^{-2 pi i (k s / L + q'/n)}, s = R/n
-template <int R, int TSTRIDE>
-__device__ __forceinline__ void tw_tab_fill(c32* tab, int k, int L) {
-  constexpr int LR = ilog2(R);
-#pragma unroll 1
-  for (int LV = 1; LV <= LR; ++LV) {
-    const int n = 1 << LV, s = R >> LV, nq = tw_nq(LV);
-    for (int qp = 0; qp < nq; ++qp) {
-      double sn, cs;
-      sincospi(-2.0 * ((double)k * s / L + (double)qp / n), &sn, &cs);
-      tab[(tw_tab_off(LV) + qp) * TSTRIDE] = mk((float)cs, (float)sn);
-    }
-  }
 }
 
 // --------------------------------------------------------------- engine

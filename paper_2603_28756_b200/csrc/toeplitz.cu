@@ -582,21 +582,16 @@ k_cols_conv64(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ 
   using S = FftShape<M, E>;
   static_assert(S::NP == 2 && (1 << S::LFIRST) == TT, "two passes, pass-0 radix == TT");
   constexpr int R0 = TT, ST0 = E / R0;
-  constexpr int TWW = tw_tab_words<E>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int g = threadIdx.x / TT, t = threadIdx.x - g * TT;
   c32* pq_s = reinterpret_cast<c32*>(smem_raw);                  // [M]
   float* bi_s = reinterpret_cast<float*>(pq_s + M);                // [M]
   c32* xb = reinterpret_cast<c32*>(bi_s + M) + g * XW;             // [G][XW]
-  c32* twt = reinterpret_cast<c32*>(bi_s + M) + G * XW;  // pass-1 step twiddles [TWW][TT]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(twt + TWW * TT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<c32*>(bi_s + M) + G * XW);
   uint64_t* full = bars + 2 * g;
   uint64_t* empty = full + 1;
   uint64_t* psf_full = bars + 2 * G;
   const int bar_id = 1 + g;
-  // pass 1 of thread t twiddles by w = e^{-2 pi i t / M}: its fold's step twiddles
-  // depend on t only, so they are tabulated once per CTA (fp64, rounded once)
-  if (g == 0) tw_tab_fill<E, TT>(twt + t, t, M);
   if (threadIdx.x == 0) mbar_init(psf_full, 1);
   if (t == 0) {
     mbar_init(full, 1);
@@ -628,7 +623,8 @@ k_cols_conv64(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ 
     tma_prefetch_desc(&tmap);
     issue();
   }
-  const c32* twp = twt + t;
+  PassTw<M, E, 1> tw;
+  tw.from_table(t);
   const long long m_stride = (long long)(TT / RB) * H * RB;
   const long long slice_stride = (long long)nrb * H * RB;
   const long long t_off = (long long)(t >> 2) * H * RB + (t & 3);
@@ -666,7 +662,7 @@ k_cols_conv64(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ 
       fft_pass<M, E, 0, false, true, false, 1>(v, (const PassTw<M, E, 0>*)nullptr);
       named_bar_sync(bar_id, TT);  // the input (in xb) has been read by the whole group
       exchange(v);
-      dft_fold_tab<E, false, false, TT>(v[0], twp);
+      fft_pass<M, E, 1, false, false, false, 1>(v, &tw);
       if (!psf_ready) {
         mbar_wait(psf_full, (uint32_t)(k & 1));
         psf_ready = true;
@@ -689,7 +685,7 @@ k_cols_conv64(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ 
         mbar_wait(empty, (uint32_t)(item & 1));
         issue();
       }
-      dft_fold_tab<E, true, true, TT>(v[0], twp);
+      fft_pass<M, E, 1, true, false, true, 1>(v, &tw);
       c32* dst = T + z * slice_stride + (long long)c * RB + t_off;
 #pragma unroll
       for (int m = 0; m < E / 2; ++m) {
@@ -994,7 +990,7 @@ int launch_cols_conv64_t(c32* T, const c32* PQ, const float* Bi, int col_len, lo
   CUtensorMap map;
   TF_TRY(encode_tmap(&map, T, M, nrb, nslices, boxr));
   const size_t smem = (sizeof(c32) + sizeof(float)) * M + sizeof(c32) * G * (size_t)(M + M / TT) +
-                      sizeof(c32) * tw_tab_words<64>() * TT + (2 * G + 1) * sizeof(uint64_t);
+                      (2 * G + 1) * sizeof(uint64_t);
   auto kern = k_cols_conv64<M, FLIP>;
   TF_TRY(prep_kernel(kern, smem));
   const int grid = std::max(1, std::min(ncols, num_sms()));

@@ -162,3 +162,22 @@ def test_repeated_apply_bitwise_stable(tf):
     ref = tf.toeplitz_apply(psf, x).clone()
     for _ in range(10):
         assert torch.equal(tf.toeplitz_apply(psf, x), ref)
+
+
+@pytest.mark.parametrize("n,nd,z", [(700, 700, 1), (700, 701, 2), (1000, 1024, 5),
+                                    (1400, 1400, 3), (1400, 1401, 6)])
+def test_apply_radix64_columns_vs_oracle(tf, n, nd, z):
+    """The two-pass radix-64 column kernel (k_cols_conv64: M = 2048 for 640 < N <= 1024,
+    M = 4096 for 1280 < N <= 2048): slice counts that leave some of its four
+    per-CTA slice groups idle or unevenly loaded (z = 1, 2, 3, 5, 6), even and odd Nd."""
+    import oracle as O
+
+    ang = np.linspace(0, np.pi, 60, endpoint=False)
+    x = np.random.default_rng(n + z).standard_normal((z, n, n))
+    ref = O.apply_batch(O.build_psf(ang, nd, n), x)
+    psf = _psf(tf, ang, nd, n)
+    assert psf.fft_side == (2048 if n <= 1024 else 4096)
+    out = tf.toeplitz_apply(psf, x)
+    assert rel_l2(out, ref) < 1e-5
+    for k in range(z):  # every slice, not just the stack as a whole
+        assert rel_l2(out[k], ref[k]) < 1e-5

@@ -8,7 +8,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
   --no-e2e --no-mbir --no-c4 --no-c5 > /dev/null 2>&1
 # Toeplitz step (64 x 2048^2): skip the PSF build and warm-up applies, capture K1, K2, K3
-SWEEP_SLICES=64 timeout 900 ncu $F -k regex:'k_rows_fwd_pf|k_cols_conv_pp|k_rows_inv' -s 12 -c 3 \
+SWEEP_SLICES=64 timeout 900 ncu $F -k regex:'k_rows_fwd_pf|k_cols_conv64|k_rows_inv' -s 12 -c 3 \
   -o gpurun_out/prof_toeplitz_$TAG -f python tools/toeplitz_sweep.py > /dev/null 2>&1
 # radix-5 side (16 x 2560^2)
 SWEEP_N=2560 SWEEP_SLICES=16 timeout 900 ncu $F -k regex:'k5_rows|k5_cols_conv' -s 12 -c 3 \
