@@ -352,11 +352,12 @@ def run_ours(args, world, rank, local):
         "traffic": _ncu_traffic(dom),
         "ncu_pipes": _ncu_json("ncu_pipes.json", dom),
         "per_kernel": per_kernel,
-        "limiter_note": "k_cols_conv is bound by its FP32 pipe and its shared-memory exchanges "
-                        "together (ncu: FMA pipe 56 %, shared ld+st wavefronts 52 %, issue 43 %; "
-                        "DRAM bytes equal the algorithmic bytes; exchange-only variant 1.23 ms, "
-                        "FP-only variant 1.61 ms, full 1.99 ms); see DESIGN.md §3 and "
-                        "profiles/r02/ncu_kernels.txt",
+        "limiter_note": "k_cols_conv (k_cols_conv64: two radix-64 passes per 4096-point "
+                        "transform, one shared-memory exchange each) is FP32-bound: FP "
+                        "instructions are 66 % of its ncu stall samples, FMA pipe 63 %, issue "
+                        "44 %, DRAM bytes = algorithmic bytes; its FFMA2 floor at the measured "
+                        "0.40 FFMA2/SMSP-cycle is 1.27 ms (DESIGN.md §3, "
+                        "profiles/r02/ncu_kernels.txt, profiles/r02/ffma2_issue_microbench.txt)",
         "gradient_total": {"bytes_per_eval": total_bytes / z,
                            "achieved": total_bytes / (tot_ms / 1e3) / 1e9,
                            "frac": total_bytes / (tot_ms / 1e3) / 1e9 / peak["value"]},
