@@ -181,6 +181,9 @@ long long tf_nufft_workspace_bytes(int os, long long nslices);
  *                             each 4-row band of each 32 x 32 grid tile (entry
  *                             (tb * (os/32) + ta) * 8 + band; (os/32)^2 * 8 + 1
  *                             pointers), samples ascending
+ *   d_tile_order: int32 [(os/32)^2] order in which the tiles are launched (a
+ *             permutation; NULL = natural order); heaviest tiles first keeps
+ *             the dense centre tiles off the end of the launch
  *   d_ab     : int32 [S][2] first window index (x, y), in [0, os)
  *   d_wts    : fp32 [S][2*width] Kaiser-Bessel weights (x taps, then y taps)
  *   d_prephase: complex64 [os] = e^{-2 pi i a (N/2) / os}
@@ -189,7 +192,7 @@ long long tf_nufft_workspace_bytes(int os, long long nslices);
  * fp32 real part, or complex64 when out_complex.  Deterministic. */
 int tf_nufft_type1(const void* d_samples, long long sample_stride, long long nslices, int n,
                    int os, int width, const int* d_tile_ptr, const int* d_tile_idx,
-                   const void* d_ab, const float* d_wts, const void* d_prephase,
+                   const int* d_tile_order, const void* d_ab, const float* d_wts, const void* d_prephase,
                    const float* d_deapod, float scale, int out_complex, void* d_out, void* d_ws,
                    long long ws_bytes, void* stream);
 

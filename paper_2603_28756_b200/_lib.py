@@ -69,7 +69,7 @@ _SIGNATURES = {
     "tf_detector_rows": (_c_int, [_c_void_p, _c_ll, _c_int, _c_int, _c_void_p, _c_int, _c_int,
                                   _c_float, _c_void_p, _c_void_p]),
     "tf_nufft_workspace_bytes": (_c_ll, [_c_int, _c_ll]),
-    "tf_nufft_type1": (_c_int, [_c_void_p, _c_ll, _c_ll, _c_int, _c_int, _c_int] + [_c_void_p] * 6
+    "tf_nufft_type1": (_c_int, [_c_void_p, _c_ll, _c_ll, _c_int, _c_int, _c_int] + [_c_void_p] * 7
                        + [_c_float, _c_int, _c_void_p, _c_void_p, _c_ll, _c_void_p]),
     "tf_nufft_plan_weights": (_c_int, [_c_void_p, _c_ll, _c_int, _c_int, _c_double, _c_void_p,
                                        _c_void_p, _c_void_p]),

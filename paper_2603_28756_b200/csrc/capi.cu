@@ -145,7 +145,8 @@ int resample_axis(const float* in, float* out, long long outer, int n_src, int n
 int detector_rows(const float* rows, long long nrows, int nd, int n_angles, const void* sph,
                   int mode, int ramp, float scale, void* out, cudaStream_t st);
 int nufft_type1(const void* samples, long long s_stride, long long nslices, int n, int os, int w,
-                const int* tile_ptr, const int* tile_idx, const void* ab, const float* wts,
+                const int* tile_ptr, const int* tile_idx, const int* tile_order, const void* ab,
+                const float* wts,
                 const void* preph, const float* deapod, float scale, int cplx, void* out,
                 void* ws, size_t ws_bytes, cudaStream_t st);
 
@@ -355,7 +356,7 @@ int tf_detector_rows(const float* d_rows, long long nrows, int nd, int n_angles,
 
 int tf_nufft_type1(const void* d_samples, long long sample_stride, long long nslices, int n,
                    int os, int width, const int* d_tile_ptr, const int* d_tile_idx,
-                   const void* d_ab, const float* d_wts, const void* d_prephase,
+                   const int* d_tile_order, const void* d_ab, const float* d_wts, const void* d_prephase,
                    const float* d_deapod, float scale, int out_complex, void* d_out, void* d_ws,
                    long long ws_bytes, void* stream) {
   TF_TRY(ensure_init());
@@ -364,7 +365,8 @@ int tf_nufft_type1(const void* d_samples, long long sample_stride, long long nsl
   if (!d_samples || !d_tile_ptr || !d_tile_idx || !d_ab || !d_wts || !d_prephase || !d_deapod ||
       !d_out || !d_ws)
     return fail_arg("null pointer");
-  return nufft_type1(d_samples, sample_stride, nslices, n, os, width, d_tile_ptr, d_tile_idx, d_ab,
+  return nufft_type1(d_samples, sample_stride, nslices, n, os, width, d_tile_ptr, d_tile_idx,
+                     d_tile_order, d_ab,
                      d_wts, d_prephase, d_deapod, scale, out_complex, d_out, d_ws,
                      (size_t)ws_bytes, (cudaStream_t)stream);
 }

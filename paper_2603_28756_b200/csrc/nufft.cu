@@ -186,10 +186,12 @@ template <int W, int NB>
 __global__ void __launch_bounds__(256)
 k_spread(const c32* __restrict__ c, long long c_stride, int nslices, int os, int ntile_a,
          const int* __restrict__ tile_ptr, const int* __restrict__ tile_idx,
-         const int2* __restrict__ ab, const float* __restrict__ wts, const c32* __restrict__ preph,
-         c32* __restrict__ grid) {
+         const int* __restrict__ tile_order, const int2* __restrict__ ab,
+         const float* __restrict__ wts, const c32* __restrict__ preph, c32* __restrict__ grid) {
   __shared__ SpreadStage<W, NB> stage_all[8];
-  const int tile = blockIdx.x;
+  // heaviest tiles first (longest-processing-time order): the polar sampling puts
+  // most samples in the centre tiles, which otherwise finish last and leave a tail
+  const int tile = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
   const int ta = tile % ntile_a, tb = tile / ntile_a;
   const int z0 = blockIdx.y * NB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -546,25 +548,28 @@ struct NufftFftFn {
 
 template <int W>
 int launch_spread(const c32* c, long long c_stride, long long nz, int os, const int* tile_ptr,
-                  const int* tile_idx, const int2* ab, const float* wts, const c32* preph,
-                  c32* grid, cudaStream_t st) {
+                  const int* tile_idx, const int* tile_order, const int2* ab, const float* wts,
+                  const c32* preph, c32* grid, cudaStream_t st) {
 #ifndef TF_SPREAD_NB
 #define TF_SPREAD_NB 2
 #endif
   constexpr int NB = TF_SPREAD_NB;  // slices per CTA: amortises each sample's index chain
   const int nta = os / 32;
   const dim3 g((unsigned)(nta * nta), (unsigned)((nz + NB - 1) / NB));
-  k_spread<W, NB><<<g, 256, 0, st>>>(c, c_stride, (int)nz, os, nta, tile_ptr, tile_idx, ab, wts,
-                                      preph, grid);
+  k_spread<W, NB><<<g, 256, 0, st>>>(c, c_stride, (int)nz, os, nta, tile_ptr, tile_idx,
+                                      tile_order, ab, wts, preph, grid);
   return check_launch("k_spread");
 }
 
 int dispatch_spread(int w, const c32* c, long long c_stride, long long nz, int os,
-                    const int* tile_ptr, const int* tile_idx, const int2* ab, const float* wts,
-                    const c32* preph, c32* grid, cudaStream_t st) {
+                    const int* tile_ptr, const int* tile_idx, const int* tile_order,
+                    const int2* ab, const float* wts, const c32* preph, c32* grid,
+                    cudaStream_t st) {
   switch (w) {
-#define TF_W(W) \
-  case W: return launch_spread<W>(c, c_stride, nz, os, tile_ptr, tile_idx, ab, wts, preph, grid, st);
+#define TF_W(W)                                                                              \
+  case W:                                                                                    \
+    return launch_spread<W>(c, c_stride, nz, os, tile_ptr, tile_idx, tile_order, ab, wts, preph, \
+                            grid, st);
     TF_W(2) TF_W(3) TF_W(4) TF_W(5) TF_W(6) TF_W(7) TF_W(8) TF_W(9) TF_W(10) TF_W(11) TF_W(12)
     TF_W(13) TF_W(14) TF_W(15) TF_W(16)
 #undef TF_W
@@ -685,7 +690,8 @@ int detector_rows(const float* rows, long long nrows, int nd, int n_angles, cons
 }
 
 int nufft_type1(const void* samples, long long s_stride, long long nslices, int n, int os, int w,
-                const int* tile_ptr, const int* tile_idx, const void* ab, const float* wts,
+                const int* tile_ptr, const int* tile_idx, const int* tile_order, const void* ab,
+                const float* wts,
                 const void* preph, const float* deapod, float scale, int cplx, void* out,
                 void* ws, size_t ws_bytes, cudaStream_t st) {
   if (!is_pow2(os) || os < 32 || os > 8192) return fail_arg("NUFFT grid side %d unsupported", os);
@@ -699,7 +705,8 @@ int nufft_type1(const void* samples, long long s_stride, long long nslices, int 
     c32* grid = reinterpret_cast<c32*>(ws);
     c32* Tn = grid + nz * plane;
     TF_TRY(dispatch_spread(w, reinterpret_cast<const c32*>(samples) + z0 * s_stride, s_stride, nz,
-                           os, tile_ptr, tile_idx, reinterpret_cast<const int2*>(ab), wts,
+                           os, tile_ptr, tile_idx, tile_order, reinterpret_cast<const int2*>(ab),
+                           wts,
                            reinterpret_cast<const c32*>(preph), grid, st));
     const size_t osz = cplx ? sizeof(c32) : sizeof(float);
     TF_TRY(dispatch_grid_fft(os, grid, Tn, nz, n, deapod, scale, cplx != 0,
