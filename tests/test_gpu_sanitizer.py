@@ -26,10 +26,13 @@ def _sanitizer():
 
 
 # N = 128 runs the generic kernels; N = 512 the TMA / bulk-copy / 256-bit paths and
-# interior K4/K5 tiles
-@pytest.mark.parametrize("tool,n", [("memcheck", 128), ("memcheck", 512), ("racecheck", 128),
-                                    ("racecheck", 512), ("synccheck", 512)])
-def test_kernels_clean_under_sanitizer(tool, n):
+# interior K4/K5 tiles; N = 1024 "toeplitz" the radix-64 column kernel (M = 2048)
+@pytest.mark.parametrize("tool,n,mode", [("memcheck", 128, ""), ("memcheck", 512, ""),
+                                         ("racecheck", 128, ""), ("racecheck", 512, ""),
+                                         ("synccheck", 512, ""), ("memcheck", 1024, "toeplitz"),
+                                         ("racecheck", 1024, "toeplitz"),
+                                         ("synccheck", 1024, "toeplitz")])
+def test_kernels_clean_under_sanitizer(tool, n, mode):
     import torch
 
     if not torch.cuda.is_available():
@@ -37,7 +40,7 @@ def test_kernels_clean_under_sanitizer(tool, n):
     exe = _sanitizer()
     if exe is None:
         pytest.skip("compute-sanitizer not found")
-    env = dict(os.environ, SAN_N=str(n), PYTHONPATH=str(ROOT))
+    env = dict(os.environ, SAN_N=str(n), SAN_MODE=mode, PYTHONPATH=str(ROOT))
     cmd = [exe, "--tool", tool, "--print-limit", "20", sys.executable,
            str(ROOT / "tools" / "sanitize.py")]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)

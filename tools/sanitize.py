@@ -11,6 +11,19 @@ import paper_2603_28756_b200 as tf  # noqa: E402
 from paper_2603_28756_b200.radon import back_project_stack, fbp_stack, forward_project_stack  # noqa: E402
 
 n = int(os.environ.get("SAN_N", "256"))
+if os.environ.get("SAN_MODE") == "toeplitz":
+    # the Toeplitz chain alone (N = 1024: the two-pass radix-64 column kernel on
+    # M = 2048 with its named barriers, mbarriers and TMA), even and odd Nd, 5 slices
+    # (uneven over the kernel's four slice groups)
+    ang = np.linspace(0, np.pi, 16, endpoint=False)
+    for nd in (n, n + 1):
+        geom = tf.ScanGeometry(angles=ang, detector_bins=nd, image_side=n)
+        psf = tf.build_psf(tf.polar_sampling(geom), n)
+        x = torch.randn((5, n, n), device="cuda")
+        y = tf.toeplitz_apply(psf, x)
+    torch.cuda.synchronize()
+    print("sanitize workload done", float(y.abs().sum()))
+    sys.exit(0)
 ang = np.linspace(0, np.pi, 24, endpoint=False)
 geom = tf.ScanGeometry(angles=ang, detector_bins=n, image_side=n)
 plan = tf.NufftPlan(n, tf.polar_sampling(geom), 1e-6)
