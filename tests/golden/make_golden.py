@@ -397,8 +397,25 @@ def fileio_fixtures():
     print("fileio fixtures written")
 
 
+def bench_csvs():
+    """The reference's bench categories at small sizes (CSV files as the reference
+    writes them): toeplitz (direct vs Toeplitz) and init (FBP vs zero)."""
+    sys.path.insert(0, str(REF))
+    from tomoforge import bench as rb
+
+    out = OUT / "bench"
+    out.mkdir(exist_ok=True)
+    rb.bench_toeplitz(out / "toeplitz.csv", sizes=(32, 48), n_angles=20, seed=0, repeats=1)
+    rb.bench_init(out / "init.csv", side=64, n_angles=30, max_iters=20, seed=7)
+    rb.bench_multires(out / "multires.csv", side=64, n_angles=30, single_iters=40,
+                      fine_iters=8, seed=7)
+    print("bench csv fixtures written")
+
+
 if __name__ == "__main__":
-    if "--only-c2" in sys.argv:
+    if "--only-bench" in sys.argv:
+        bench_csvs()
+    elif "--only-c2" in sys.argv:
         c2_reduced()
     elif "--only-fileio" in sys.argv:
         fileio_fixtures()

@@ -28,3 +28,14 @@ def test_exit_codes(tmp_path, monkeypatch):
     monkeypatch.setenv("TOMOFORGE_THREADS", "many")
     assert cli.main(["phantom", "--kind", "disk", "--side", "8", "--radius", "9",
                      "--out", str(tmp_path / "d.raw")]) == cli.EXIT_USAGE
+
+
+def test_bench_options_match_reference():
+    """`bench` takes the reference's categories and options (cli.py:223-233)."""
+    from paper_2603_28756_b200 import cli
+
+    ap = cli.build_parser()
+    for cat in ("toeplitz", "init", "multires", "scaling"):
+        a = ap.parse_args(["bench", cat, "--out", "x.csv"])
+        assert a.category == cat and a.sizes == [32, 64, 128, 256] and a.side == 256
+        assert a.slices == 32 and a.angles == 60 and a.iters == 3 and a.workers == [1, 2, 4]
