@@ -453,6 +453,7 @@ def _mbir(tf, args, world, rank):
     psf, t_psf = timed(lambda: tf.build_psf(plan.sampling, N_SIDE))
     ctx, t_rstar = timed(lambda: tf.fidelity_context(plan, psf, sino))
     f0, t_fbp = timed(lambda: fbp_stack(plan, g))
+    direct = _direct_vs_toeplitz(tf, plan, psf, ctx, g, z, timed)
     L = tf.estimate_lipschitz(psf, prm)
     iters = 10
     cfg = tf.SolverConfig(max_iters=iters, tol=1e-300, lipschitz=L)
@@ -495,6 +496,7 @@ def _mbir(tf, args, world, rank):
     return {
         "workload": f"C3 slab: {z} x 2048^2 per GPU, 128 angles, Nd=2048, qGGMRF lam=5e-4",
         "slab256_iteration": slab,
+        "direct_vs_toeplitz": direct,
         "c1_end_to_end": c1,
         "setup_ms": {"psf": t_psf, "rstar_nufft": t_rstar, "fbp_nufft": t_fbp},
         "solve_ms_per_iter": per_it,
@@ -507,6 +509,36 @@ def _mbir(tf, args, world, rank):
                                  "Lanczos-3 upsampling, L fixed from the finest level; "
                                  "second call (cold = first call of the process)",
     }
+
+
+def _direct_vs_toeplitz(tf, plan, psf, ctx, g, z, timed):
+    """The paper's Fig. 2 comparison (reference bench.py:46-86) at the bench size: the
+    fidelity gradient R*(R f - g) by the direct projection pair (GPU type-2 forward
+    projector, then the type-1 back-projector) vs the Toeplitz route K f - R*g, on
+    the same 64 x 2048^2 device slab; times per slab and the relative difference."""
+    import torch
+
+    from paper_2603_28756_b200.radon import back_project_stack, forward_project_stack
+    from paper_2603_28756_b200.toeplitz import apply_stack
+
+    f = torch.randn((z, N_SIDE, N_SIDE), generator=torch.Generator("cuda").manual_seed(6),
+                    device="cuda")
+    rows = torch.from_numpy(g.astype(np.float32)).cuda()
+
+    def direct():
+        return back_project_stack(plan, forward_project_stack(plan, f) - rows)
+
+    def toep():
+        return apply_stack(psf, f, aux=ctx.rstar, alpha=1.0, beta=-1.0)
+
+    direct(), toep()  # warm
+    gd, t_direct = timed(direct)
+    gt, t_toep = timed(toep)
+    rel = float(torch.linalg.vector_norm(gt - gd) / torch.linalg.vector_norm(gd))
+    return {"slices": z, "direct_ms": t_direct, "toeplitz_ms": t_toep,
+            "speedup": t_direct / t_toep, "rel_diff_grad": rel,
+            "direct": "forward_project_stack (type 2) then back_project_stack (type 1)",
+            "toeplitz": "apply_stack(psf, f, aux=R*g, beta=-1) (K1/K2/K3)"}
 
 
 def _c1_pipeline(tf, timed):
