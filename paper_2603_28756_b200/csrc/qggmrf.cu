@@ -316,9 +316,12 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* K
 }
 
 // every TF_XRCP_K4-th (K5: TF_XRCP_K5-th) clique pair of the tiled kernels takes its
-// reciprocal on the XU, balancing XU against issue (measured: K4 3 -> -2.5 %, K5 none)
+// reciprocal on the XU, balancing XU against issue.  The gradient part of K45 uses
+// the same choice (its update must equal K4's bit for bit), and K45's XU also
+// carries the energy's transcendentals: 6 is best for K45 (measured on 64 x 2048^2:
+// K45 5.36 ms at 3, 5.32 at 6, 5.35 with none; K4 alone 3.15 / 3.17 / 3.20)
 #ifndef TF_XRCP_K4
-#define TF_XRCP_K4 3
+#define TF_XRCP_K4 6
 #endif
 #ifndef TF_XRCP_K5
 #define TF_XRCP_K5 0
