@@ -228,9 +228,12 @@ int upsample3(const float* src, int zs, int hs, int ws, float* out, int t_begin,
   TF_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem),
                     "occupancy"));
   const int gx = (wt + UP_TX - 1) / UP_TX, gy = (ht + UP_TY - 1) / UP_TY;
-  // split the target planes only when the tiles alone cannot fill ~2 waves
+  // split the target planes into z-runs so that the launch is ~16 waves of CTAs: with
+  // one run per tile (1024 tiles at 2048^2) the last partial wave of long runs left
+  // two thirds of the SMs idle for a third of the kernel; each extra run re-reads
+  // only its first kz coarse window planes
   const long long tiles = (long long)gx * gy;
-  const long long want = 2LL * std::max(1, per_sm) * num_sms();
+  const long long want = 16LL * std::max(1, per_sm) * num_sms();
   const int zch = (int)std::max<long long>(1, std::min<long long>(nzt, (want + tiles - 1) / tiles));
   const int zper = (nzt + zch - 1) / zch;
   const dim3 g(gx, gy, (nzt + zper - 1) / zper);
