@@ -297,8 +297,8 @@ def run_ours(args, world, rank, local):
 
     dev = torch.device("cuda", torch.cuda.current_device())
     # C4 first, on a clean device (R*g + 4 volumes of 2048^3 take ~175 of 191 GB)
-    c4 = None if args.no_c4 else _c4(args, world, rank)
-    c5 = None if args.no_c5 else _c5(args, world, rank)
+    c4 = None if args.no_c4 else _leg(_c4, args, world, rank)
+    c5 = None if args.no_c5 else _leg(_c5, args, world, rank)
     z = args.slices
     geom = tf.ScanGeometry(angles=angles(), detector_bins=N_BINS, image_side=N_SIDE)
     psf = tf.build_psf(tf.polar_sampling(geom), N_SIDE)
@@ -365,11 +365,11 @@ def run_ours(args, world, rank, local):
 
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(tf, ctx, z, world, args.e2e_steps)
+        e2e = _leg(_e2e, tf, ctx, z, world, args.e2e_steps)
     mbir = None
     if not args.no_mbir:
         del out
-        mbir = _mbir(tf, args, world, rank)
+        mbir = _leg(_mbir, tf, args, world, rank)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         psf_o, _, _, threads, slices, times = cpu_sample()
@@ -390,6 +390,22 @@ def run_ours(args, world, rank, local):
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
+
+
+def _leg(fn, *a):
+    """A secondary measurement: its failure is recorded in the JSON line (traceback on
+    stderr) instead of taking the headline measurement down with it."""
+    import traceback
+
+    import torch
+
+    try:
+        return fn(*a)
+    except Exception as exc:  # noqa: BLE001
+        traceback.print_exc()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        return {"error": f"{type(exc).__name__}: {exc}"}
 
 
 def _make_context(tf, psf, geom, z, rank):
