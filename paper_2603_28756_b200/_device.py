@@ -67,10 +67,12 @@ def as_stack(f, what: str = "input"):
     raise ValueError(f"{what} must be 2D or 3D, got shape {arr.shape}")
 
 
-_CHUNK_ELEMS = 1 << 25  # 256 MB of float64 per staged copy
+_CHUNK_ELEMS = 1 << 23  # 64 MB of float64 per staged copy (32 MB page-locked fp32
+# stages: a process's first 2048^3-sinogram upload spent ~0.14 s pinning 2 x 128 MB)
 # host float64 inputs are narrowed to fp32 by the staging threads (round to
-# nearest, bit-identical to narrowing on the device, half the upload bytes)
-_STAGE_THREADS = min(8, os.cpu_count() or 1)
+# nearest, bit-identical to narrowing on the device, half the upload bytes);
+# 4.3 GB float64 -> device: 0.09 s with 8 threads, 0.08 s with 16
+_STAGE_THREADS = min(16, os.cpu_count() or 1)
 _stage_pool = None
 
 
