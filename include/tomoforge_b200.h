@@ -258,6 +258,16 @@ int tf_upsample3(const float* d_src, int zs, int hs, int ws, float* d_out, int t
 int tf_timing_enable(int on);
 int tf_timing_collect(double* ms_out, long long* n_out, int nslots);
 
+/* Peer-memory halo exchange (z-slab runtime; replaces the NCCL send/recv of
+ * runtime.exchange_halos, reference runtime.py:323-342).  After a stream-ordered
+ * peer copy of a boundary plane into a neighbour's inbox (IPC-mapped device
+ * memory), tf_halo_signal publishes `value` in the inbox slot's flag word
+ * (uint64, system-scope fence first); tf_halo_wait makes the stream wait until
+ * both flags (NULL = no neighbour) are >= value.  Single-thread kernels. */
+int tf_halo_signal(void* d_flag, unsigned long long value, void* stream);
+int tf_halo_wait(const void* d_flag_lo, const void* d_flag_hi, unsigned long long value,
+                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,8 @@ _SIGNATURES = {
     "tf_nufft_workspace_bytes": (_c_ll, [_c_int, _c_ll]),
     "tf_nufft_type1": (_c_int, [_c_void_p, _c_ll, _c_ll, _c_int, _c_int, _c_int] + [_c_void_p] * 7
                        + [_c_float, _c_int, _c_void_p, _c_void_p, _c_ll, _c_void_p]),
+    "tf_halo_signal": (_c_int, [_c_void_p, ctypes.c_ulonglong, _c_void_p]),
+    "tf_halo_wait": (_c_int, [_c_void_p, _c_void_p, ctypes.c_ulonglong, _c_void_p]),
     "tf_nufft_plan_weights": (_c_int, [_c_void_p, _c_ll, _c_int, _c_int, _c_double, _c_void_p,
                                        _c_void_p, _c_void_p]),
     "tf_nufft_type2_workspace_bytes": (_c_ll, [_c_int, _c_int, _c_ll]),

@@ -150,6 +150,10 @@ int nufft_type1(const void* samples, long long s_stride, long long nslices, int 
                 const void* preph, const float* deapod, float scale, int cplx, void* out,
                 void* ws, size_t ws_bytes, cudaStream_t st);
 
+int halo_signal(unsigned long long* flag, unsigned long long value, cudaStream_t st);
+int halo_wait(const unsigned long long* flag_lo, const unsigned long long* flag_hi,
+              unsigned long long value, cudaStream_t st);
+
 }  // namespace tf
 
 using namespace tf;
@@ -463,6 +467,21 @@ int tf_timing_collect(double* ms_out, long long* n_out, int nslots) {
     n_out[i] = g_time_n[i];
   }
   return TF_OK;
+}
+
+
+int tf_halo_signal(void* d_flag, unsigned long long value, void* stream) {
+  TF_TRY(ensure_init());
+  if (!d_flag) return fail_arg("null flag");
+  return halo_signal(reinterpret_cast<unsigned long long*>(d_flag), value, (cudaStream_t)stream);
+}
+
+int tf_halo_wait(const void* d_flag_lo, const void* d_flag_hi, unsigned long long value,
+                 void* stream) {
+  TF_TRY(ensure_init());
+  return halo_wait(reinterpret_cast<const unsigned long long*>(d_flag_lo),
+                   reinterpret_cast<const unsigned long long*>(d_flag_hi), value,
+                   (cudaStream_t)stream);
 }
 
 }  // extern "C"

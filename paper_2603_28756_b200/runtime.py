@@ -137,14 +137,18 @@ class SlabComm:
     test_runtime.py:239-250).
     """
 
-    def __init__(self, part: SlabPartition, group=None):
+    def __init__(self, part: SlabPartition, group=None, halo: str = "nccl"):
         self.part = part
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         if self.rank != part.worker_id:
             raise ProtocolError(f"rank {self.rank} given the partition of worker {part.worker_id}")
+        if halo not in ("nccl", "peer"):
+            raise ValueError("halo must be 'nccl' or 'peer'")
         self.direct = dist.get_backend(group) == "nccl"
+        self.halo = halo
+        self._peer_halo = None  # _PeerHalo, created at the first exchange (plane shape known)
         self.counts = collections.Counter()
 
     def _peer(self, w):
@@ -161,6 +165,11 @@ class SlabComm:
         part = self.part
         if slab.shape[0] != part.size:
             raise ProtocolError(f"slab has {slab.shape[0]} slices, partition owns {part.size}")
+        if self.halo == "peer" and slab.is_cuda:
+            if self._peer_halo is None:
+                self._peer_halo = _PeerHalo(self, tuple(slab.shape[1:]), slab.dtype, slab.device)
+            self.counts["halo"] += (part.lower is not None) + (part.upper is not None)
+            return self._peer_halo.start(slab)
         plane_shape = slab.shape[1:]
         staged = not (self.direct and slab.is_cuda)
         buf_dev = "cpu" if staged else slab.device
@@ -192,6 +201,8 @@ class SlabComm:
         return reqs, lo, hi
 
     def exchange_finish(self, handle):
+        if isinstance(handle, _PeerTicket):
+            return self._peer_halo.finish(handle)
         reqs, lo, hi = handle
         for req in reqs:
             req.wait()
@@ -270,6 +281,65 @@ class SlabComm:
         return torch.cat([bufs[p.worker_id][:p.size] for p in parts])
 
 
+@dataclass(frozen=True)
+class _PeerTicket:
+    parity: int
+    value: int
+
+
+class _PeerHalo:
+    """Halo planes written straight into the neighbours' device memory (csrc/halo.cu).
+
+    Each rank's inbox -- [parity][lo, hi] planes plus a uint64 flag per slot -- is
+    shared once over the group (CUDA IPC handles, all_gather_object) and mapped by
+    the neighbours, over NVLink when they are other GPUs of the node.  ``start``
+    copies this slab's first / last plane into the lower / upper neighbour's slot
+    (stream-ordered peer copies) and publishes the exchange number there
+    (tf_halo_signal); ``finish`` makes the stream wait for both neighbours' flags
+    (tf_halo_wait) and returns views of its own inbox.  Two parity slots suffice
+    because the per-iteration scalar allreduce keeps the ranks in lockstep."""
+
+    def __init__(self, comm: "SlabComm", plane_shape, dtype, device):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.comm, self.part = comm, comm.part
+        self.inbox = torch.zeros((2, 2) + tuple(plane_shape), dtype=dtype, device=device)
+        self.flags = torch.zeros((2, 2), dtype=torch.int64, device=device)
+        mine = (reduce_tensor(self.inbox), reduce_tensor(self.flags))
+        objs = [None] * comm.world
+        dist.all_gather_object(objs, mine, group=comm.group)
+        self.peer = {}
+        for q in (self.part.lower, self.part.upper):
+            if q is not None:
+                (f_in, a_in), (f_fl, a_fl) = objs[q]
+                self.peer[q] = (f_in(*a_in), f_fl(*a_fl))
+        self.count = 0
+
+    def start(self, slab: torch.Tensor) -> _PeerTicket:
+        lib = _lib.ensure_ready()
+        k = self.count
+        self.count += 1
+        p, value = k & 1, k + 1
+        st = _lib.stream_handle()
+        for q, plane, side in ((self.part.lower, slab[0], 1), (self.part.upper, slab[-1], 0)):
+            if q is None:
+                continue
+            inbox, flags = self.peer[q]
+            inbox[p, side].copy_(plane, non_blocking=True)  # my boundary = q's halo
+            _lib.check(lib.tf_halo_signal(flags[p, side].data_ptr(), value, st),
+                       "tf_halo_signal")
+        return _PeerTicket(p, value)
+
+    def finish(self, t: _PeerTicket):
+        lib = _lib.ensure_ready()
+        lo_ok, hi_ok = self.part.lower is not None, self.part.upper is not None
+        _lib.check(lib.tf_halo_wait(self.flags[t.parity, 0].data_ptr() if lo_ok else None,
+                                    self.flags[t.parity, 1].data_ptr() if hi_ok else None,
+                                    t.value, _lib.stream_handle()), "tf_halo_wait")
+        return (self.inbox[t.parity, 0] if lo_ok else None,
+                self.inbox[t.parity, 1] if hi_ok else None)
+
+
 class _Rows:
     """The sinogram a slab solve reads from: a ``Sinogram``, or the path of a saved
     one (fileio format), memory-mapped so that each rank touches only its own rows
@@ -302,7 +372,7 @@ class _Rows:
 def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig, n_workers: int,
                       *, f0: Volume | None = None, transport=None, nufft_tolerance: float = 1e-6,
                       oversampling: float = 2.0, on_record=None, snapshot_sink=None,
-                      gather: str = "root", group=None):
+                      gather: str = "root", group=None, halo: str = "nccl"):
     """Slab-parallel reconstruction, algebraically identical to ``solve`` (runtime.py:622-691).
 
     SPMD: every rank of the process group (one per GPU, ``n_workers`` = group
@@ -313,7 +383,9 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
     0 only (snapshots gather the full volume every iteration -- tests only).
     ``transport`` is accepted for signature compatibility; the transport is the
     process group.  ``sino`` may also be the path of a saved sinogram: each rank
-    then reads only its own rows (memory-mapped).
+    then reads only its own rows (memory-mapped).  ``halo="peer"`` writes the halo
+    planes straight into the neighbours' device memory (IPC-mapped inboxes,
+    csrc/halo.cu) instead of sending them over the group.
     """
     src = _Rows(sino)
     if n_workers < 1:
@@ -352,7 +424,7 @@ def distributed_solve(sino: Sinogram, image_side: int, params, cfg: SolverConfig
     rank = dist.get_rank(group)
     parts = partition(src.slices, n_workers)
     part = parts[rank]
-    comm = SlabComm(part, group)
+    comm = SlabComm(part, group, halo=halo)
     try:
         L = cfg.lipschitz
         if L is None:
@@ -390,7 +462,8 @@ def distributed_solve_hierarchical(full_sino: Sinogram, hierarchy, params, cfg: 
                                    n_workers: int, *, use_fbp_init: bool = False,
                                    downsample_angles: bool = False,
                                    nufft_tolerance: float = 1e-6, oversampling: float = 2.0,
-                                   on_record=None, gather: str = "root", group=None):
+                                   on_record=None, gather: str = "root", group=None,
+                                   halo: str = "nccl"):
     """Coarse-to-fine schedule over z-slabs (multires.py:198-242 x runtime.py:622-691).
 
     The reference never combines the two (cli.py:104-131); the north-star C4/C5
@@ -447,7 +520,7 @@ def distributed_solve_hierarchical(full_sino: Sinogram, hierarchy, params, cfg: 
         sampling = polar_sampling(geom)
         plan = NufftPlan(side, sampling, nufft_tolerance, oversampling)
         psf = build_psf(sampling, side, nufft_tolerance, oversampling)
-        comm = SlabComm(part, group)
+        comm = SlabComm(part, group, halo=halo)
         L = cfg.lipschitz
         if L is None:
             L = comm.broadcast_scalar(estimate_lipschitz(psf, params) if rank == 0 else None)

@@ -141,3 +141,37 @@ def diverge_worker(rank, world, port, fixture, out_dir):
             fh.write(msg)
     finally:
         dist.destroy_process_group()
+
+
+def peer_halo_worker(rank, world, port, out_dir):
+    """distributed_solve (3-D, 9 slices over `world` ranks on cuda:0, gloo control plane)
+    with the halo planes sent over the group ("nccl" path: host-staged on gloo) and
+    written into the neighbours' IPC-mapped inboxes ("peer"); plus the hierarchical
+    solve with peer halos."""
+    import paper_2603_28756_b200 as tf
+    from paper_2603_28756_b200.runtime import distributed_solve, distributed_solve_hierarchical
+
+    torch.cuda.set_device(0)
+    _init(rank, world, port)
+    try:
+        ang = np.linspace(0, np.pi, 12, endpoint=False)
+        g = np.random.default_rng(9).standard_normal((9, 12, 24))
+        sino = tf.Sinogram(angles=ang, data=g)
+        prm = tf.QggmrfParams(sigma=0.3, lam=0.05)
+        cfg = tf.SolverConfig(max_iters=7, tol=1e-300, lipschitz=300.0)
+        res = {}
+        for halo in ("nccl", "peer"):
+            vol, recs = distributed_solve(sino, 24, prm, cfg, world, halo=halo)
+            if rank == 0:
+                res[halo] = (vol.data, np.array([r.objective for r in recs]))
+        hier = tf.GridHierarchy(levels=(12, 24), iters_per_level=(4, 3))
+        for halo in ("nccl", "peer"):
+            vol, lrecs = distributed_solve_hierarchical(
+                sino, hier, prm, tf.SolverConfig(max_iters=1, tol=1e-300), world,
+                use_fbp_init=True, halo=halo)
+            if rank == 0:
+                res["hier_" + halo] = (vol.data, np.array([r.objective for r in lrecs[-1]]))
+        if rank == 0:
+            np.save(os.path.join(out_dir, f"peer_w{world}.npy"), res, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()

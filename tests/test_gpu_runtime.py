@@ -98,3 +98,22 @@ def test_worker_divergence_is_runtime_error(tf, tmp_path):
     for rank in range(2):
         msg = (tmp_path / f"diverge{rank}.txt").read_text()
         assert msg.startswith("RuntimeError") and "worker" in msg and "non-finite" in msg
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_memory_halos_match_group_halos(tf, tmp_path, world):
+    """halo="peer" (planes copied into the neighbours' IPC-mapped inboxes, flag
+    published / awaited by tf_halo_signal / tf_halo_wait) gives bit-for-bit the
+    reconstruction of the group send/recv path, for plain and hierarchical solves."""
+    import torch.multiprocessing as mp
+
+    from _dist_workers import peer_halo_worker
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(peer_halo_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    r = np.load(tmp_path / f"peer_w{world}.npy", allow_pickle=True).item()
+    for a, b in (("nccl", "peer"), ("hier_nccl", "hier_peer")):
+        np.testing.assert_array_equal(r[a][0], r[b][0])
+        np.testing.assert_array_equal(r[a][1], r[b][1])
