@@ -742,22 +742,29 @@ __global__ void k_psf_lags(float* __restrict__ kmain, float* __restrict__ kflip,
   const int i0 = (int)(id / M), i1 = (int)(id - (long long)i0 * M);
   const int d0 = i0 < n ? i0 : i0 - M;
   const int d1 = i1 < n ? i1 : i1 - M;
-  float km = 0.f, kf = 0.f;
-  if (d0 > -n && d1 > -n && (i0 < n || i0 > M - n) && (i1 < n || i1 > M - n)) {
-    const int jlo = -(nd / 2), jhi = (nd + 1) / 2 - 1;
-    const bool even = (nd % 2) == 0;
-    double k = 0.0, kn = 0.0;
-    for (int a = 0; a < n_angles; ++a) {
-      const double u = d0 * cs[2 * a] + d1 * cs[2 * a + 1];
-      k += dirichlet(u, nd, jlo, jhi);
-      if (even) kn += cospi(u);
-    }
-    kn *= 0.5;
-    km = (float)((k - kn) / nd);
-    kf = (float)(-kn / nd);
+  if (!(d0 > -n && d1 > -n && (i0 < n || i0 > M - n) && (i1 < n || i1 > M - n))) {
+    kmain[id] = 0.f;  // outside the lag support |d| <= n - 1
+    kflip[id] = 0.f;
+    return;
   }
+  // K(-d) = K(d) (D and cos are even, u(-d) = -u(d) exactly): the thread of the
+  // representative d0 > 0 or (d0 = 0, d1 >= 0) writes both lags -- half the fp64 work
+  if (!(d0 > 0 || (d0 == 0 && d1 >= 0))) return;
+  const int jlo = -(nd / 2), jhi = (nd + 1) / 2 - 1;
+  const bool even = (nd % 2) == 0;
+  double k = 0.0, kn = 0.0;
+  for (int a = 0; a < n_angles; ++a) {
+    const double u = d0 * cs[2 * a] + d1 * cs[2 * a + 1];
+    k += dirichlet(u, nd, jlo, jhi);
+    if (even) kn += cospi(u);
+  }
+  kn *= 0.5;
+  const float km = (float)((k - kn) / nd), kf = (float)(-kn / nd);
+  const long long mirror = (long long)(d0 == 0 ? 0 : M - d0) * M + (d1 <= 0 ? -d1 : M - d1);
   kmain[id] = km;
   kflip[id] = kf;
+  kmain[mirror] = km;
+  kflip[mirror] = kf;
 }
 
 // The reference's lag kernel K(d) = Re type1(1 at every polar sample) on its odd
