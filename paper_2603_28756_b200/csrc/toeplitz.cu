@@ -815,6 +815,36 @@ __global__ void k_psf_finish(const c32* __restrict__ spec, c32* __restrict__ PQ,
   Bi[id] = (float)bim;
 }
 
+// 4-D tensor map over the row-blocked half spectrum: dims (fp32 units)
+// {8 = 4 rows x re/im, M/2+1 columns, nrb row blocks, nslices}; box {8, 1, boxr, 1}
+int encode_tmap(CUtensorMap* map, c32* T, int M, int nrb, long long nslices, int boxr) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    TF_TRY(check_cuda(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+                      "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)"));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return TF_ECUDA;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t H = M / 2 + 1;
+  const cuuint64_t dims[4] = {8, H, (cuuint64_t)nrb, (cuuint64_t)nslices};
+  const cuuint64_t strides[3] = {32, H * 32, H * 32 * (cuuint64_t)nrb};
+  const cuuint32_t box[4] = {8, 1, (cuuint32_t)boxr, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return TF_ECUDA;
+  }
+  return TF_OK;
+}
+
 // ============================================================ host dispatch
 namespace {
 
@@ -928,36 +958,6 @@ int launch_rows_inv(const c32* T, float* out, const float* aux, int rows, int n_
                     long long os, long long orow, float alpha, float beta, long long nslices,
                     cudaStream_t st) {
   return launch_rows_inv_t<M, 2>(T, out, aux, rows, n_out, os, orow, alpha, beta, nslices, st);
-}
-
-// 4-D tensor map over the row-blocked half spectrum: dims (fp32 units)
-// {8 = 4 rows x re/im, M/2+1 columns, nrb row blocks, nslices}; box {8, 1, boxr, 1}
-int encode_tmap(CUtensorMap* map, c32* T, int M, int nrb, long long nslices, int boxr) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    TF_TRY(check_cuda(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
-                      "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)"));
-    if (!fn || q != cudaDriverEntryPointSuccess) {
-      set_error("cuTensorMapEncodeTiled unavailable");
-      return TF_ECUDA;
-    }
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  const cuuint64_t H = M / 2 + 1;
-  const cuuint64_t dims[4] = {8, H, (cuuint64_t)nrb, (cuuint64_t)nslices};
-  const cuuint64_t strides[3] = {32, H * 32, H * 32 * (cuuint64_t)nrb};
-  const cuuint32_t box[4] = {8, 1, (cuuint32_t)boxr, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-    return TF_ECUDA;
-  }
-  return TF_OK;
 }
 
 constexpr int CONV_STAGES = 2;

@@ -15,12 +15,18 @@
 //   K3 k5_rows_inv  : a row pair's Hermitian spectrum gathered in layout G,
 //                     inverse 5Q FFT, crop, out = alpha y + beta aux.
 //   k5_cols_fwd     : forward column FFT of the PSF lag grids.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
+#include "tf_async.cuh"
 #include "tf_common.cuh"
 #include "tf_fft5.cuh"
 
 namespace tf {
+
+int encode_tmap(CUtensorMap* map, c32* T, int M, int nrb, long long nslices, int boxr);
 
 namespace {
 
@@ -200,6 +206,202 @@ k5_cols_conv(c32* __restrict__ T, const c32* __restrict__ PQ, const float* __res
   }
 }
 
+// K2 for M = 5120 (Q = 1024, the C5 finest level) in the style of k_cols_conv64:
+// a group of five warps per (column, slice) item, three groups per CTA, one CTA per
+// SM.  With n = n1 + Q n2 and k = 5 k1 + k2 (tf_fft5.cuh):
+// * layout I (128 threads, eight n1 each): the radix-5 step over n2 with the
+//   W_M^{n1 k2} twiddles, written to sub-buffer k2 at word n1 + n1/32;
+// * layout G (warp k2 of the group, lane t): the Q-point transform of z_k2 as two
+//   radix-32 passes (E = 32) whose one exchange stays inside the warp (__syncwarp);
+//   it leaves X[5 (t + 32 m) + k2] in register m for the PSF product (the column's
+//   PSF bulk-copied to shared memory once per column, shared by the groups);
+// * the inverse runs the same way back, then the inverse radix-5 step in layout I
+//   writes the kept outputs n < N straight to the half spectrum.
+// Three group barriers per item instead of the ~10 CTA barriers and six exchanges
+// of k5_cols_conv; the next item is TMA-gathered into the group's buffer as soon as
+// the last exchange has been read.
+template <bool FLIP, int G>
+__global__ void __launch_bounds__(G * 160, 1)
+k5_cols_conv_q1024(const __grid_constant__ CUtensorMap tmap, const c32* __restrict__ PQ,
+                   const float* __restrict__ Bi, int ncols, int nrb, int nslices, int boxr,
+                   c32* __restrict__ T) {
+  constexpr int Q = 1024, M = 5 * Q, H = M / 2 + 1, E = 32, TQ = Q / E;
+  constexpr int GT = 5 * TQ;          // 160 threads per group
+  constexpr int TI = Q / 8;           // layout I: 128 threads x 8 n1
+  constexpr int SW = Q + Q / TQ;      // sub-buffer words (pad 1 per 32)
+  constexpr int XW = 5 * SW;          // group buffer words
+  using S = FftShape<Q, E>;
+  static_assert(S::NP == 2 && (1 << S::LFIRST) == TQ, "two radix-32 passes");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int g = threadIdx.x / GT, p = threadIdx.x - g * GT;
+  const int k2 = p / TQ, t = p - k2 * TQ;  // layout G: warp k2, lane t
+  c32* pq_s = reinterpret_cast<c32*>(smem_raw);
+  float* bi_s = reinterpret_cast<float*>(pq_s + M);
+  c32* xb = reinterpret_cast<c32*>(bi_s + M) + g * XW;
+  c32* tw5s = reinterpret_cast<c32*>(bi_s + M) + G * XW;  // W_M^{n1}, n1 < Q
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tw5s + Q);
+  uint64_t* full = bars + 2 * g;
+  uint64_t* empty = full + 1;
+  uint64_t* psf_full = bars + 2 * G;
+  const int bar_id = 1 + g;
+  // the radix-5 step's base twiddles, read 16 times per item: shared memory, not L1/L2
+  for (int i = threadIdx.x; i < Q; i += G * GT) tw5s[i] = g_tw5[(Q - Q5_MIN) + i];
+  if (threadIdx.x == 0) mbar_init(psf_full, 1);
+  if (p == 0) {
+    mbar_init(full, 1);
+    mbar_init(empty, GT);
+  }
+  if (threadIdx.x == 0) fence_mbar_init();
+  __syncthreads();
+  if ((int)blockIdx.x >= ncols) return;
+  const bool active = g < nslices;
+  const int my_cols = (ncols - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int nz_g = active ? (nslices - g + G - 1) / G : 0;
+  const int nitems = my_cols * nz_g;
+  const int nbox = (nrb + boxr - 1) / boxr;
+  const uint32_t box_bytes = (uint32_t)boxr * RB5 * sizeof(c32);
+  const int col_len = nrb * RB5;
+  int p_col = blockIdx.x, p_z = g, issued = 0;
+  auto issue = [&]() {
+    mbar_expect_tx(full, nbox * box_bytes);
+    for (int q = 0; q < nbox; ++q)
+      tma_load_4d(xb + q * boxr * RB5, &tmap, 0, p_col, q * boxr, p_z, full);
+    ++issued;
+    p_z += G;
+    if (p_z >= nslices) {
+      p_z = g;
+      p_col += gridDim.x;
+    }
+  };
+  if (p == 0 && nitems > 0) {
+    tma_prefetch_desc(&tmap);
+    issue();
+  }
+  PassTw<Q, E, 1> tw;
+  tw.from_table(t);
+  c32* sub = xb + k2 * SW;  // this warp's sub-buffer
+  // one radix-32 exchange inside the warp: pass-0 outputs of lane t are words t*32 + r
+  // (padded t*33 + r), the canonical reads t + 32 m (padded t + 33 m)
+  auto warp_exchange = [&](c32 (&v)[1][E]) {
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < E; ++r) sub[t * (TQ + 1) + r] = v[0][r];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[0][m] = sub[t + (TQ + 1) * m];
+  };
+  const long long rb_stride = (long long)H * RB5;
+  const long long slice_stride = (long long)nrb * rb_stride;
+  int item = 0;
+  for (int kc = 0; kc < my_cols; ++kc) {
+    const int c = blockIdx.x + kc * gridDim.x;
+    __syncthreads();  // every group is done with the previous column's PSF
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(psf_full, M * (uint32_t)(sizeof(c32) + (FLIP ? sizeof(float) : 0)));
+      bulk_g2s(pq_s, PQ + (long long)c * M, M * sizeof(c32), psf_full);
+      if constexpr (FLIP) bulk_g2s(bi_s, Bi + (long long)c * M, M * sizeof(float), psf_full);
+      if (kc + 1 < my_cols) {
+        bulk_prefetch_l2(PQ + (long long)(c + gridDim.x) * M, M * sizeof(c32));
+        if constexpr (FLIP) bulk_prefetch_l2(Bi + (long long)(c + gridDim.x) * M, M * sizeof(float));
+      }
+    }
+    bool psf_ready = false;
+    for (int z = g; active && z < nslices; z += G, ++item) {
+      mbar_wait(full, (uint32_t)(item & 1));
+      // ---- forward radix-5 step, layout I (the input sits in xb[0, col_len))
+      c32 a5[8][3];
+      if (p < TI) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n1 = p + TI * j;
+#pragma unroll
+          for (int n2 = 0; n2 < 3; ++n2) {
+            const int n = n1 + Q * n2;
+            a5[j][n2] = n < col_len ? xb[n] : mk(0.f, 0.f);
+          }
+        }
+      }
+      named_bar_sync(bar_id, GT);  // the input has been read: xb takes the sub-buffers
+      if (p < TI) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n1 = p + TI * j;
+          c32 a[5] = {a5[j][0], a5[j][1], a5[j][2], mk(0.f, 0.f), mk(0.f, 0.f)};
+          dft5<false>(a);
+          c32 w[5];
+          w[1] = tw5s[n1];
+          w[2] = cmul(w[1], w[1]);
+          w[3] = cmul(w[2], w[1]);
+          w[4] = cmul(w[2], w[2]);
+          const int word = n1 + n1 / TQ;
+          xb[word] = a[0];
+#pragma unroll
+          for (int kk = 1; kk < 5; ++kk) xb[kk * SW + word] = cmul(a[kk], w[kk]);
+        }
+      }
+      named_bar_sync(bar_id, GT);
+      // ---- forward Q-point transform of z_k2, layout G
+      c32 v[1][E];
+#pragma unroll
+      for (int m = 0; m < E; ++m) v[0][m] = sub[t + (TQ + 1) * m];
+      fft_pass<Q, E, 0, false, false, false, 1>(v, (const PassTw<Q, E, 0>*)nullptr);
+      warp_exchange(v);
+      fft_pass<Q, E, 1, false, false, false, 1>(v, &tw);
+      if (!psf_ready) {
+        mbar_wait(psf_full, (uint32_t)(kc & 1));
+        psf_ready = true;
+      }
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        const int kx = 5 * (t + TQ * m) + k2;
+        const c32 pq = pq_s[kx];
+        if constexpr (FLIP) {
+          const float bi = bi_s[kx];
+          v[0][m] = pfma(mk(v[0][m].y, v[0][m].x), mk(bi, bi), pmul(v[0][m], pq));
+        } else {
+          v[0][m] = pmul(v[0][m], pq);
+        }
+      }
+      // ---- inverse Q-point transform, then back to layout I
+      fft_pass<Q, E, 0, true, false, false, 1>(v, (const PassTw<Q, E, 0>*)nullptr);
+      warp_exchange(v);
+      fft_pass<Q, E, 1, true, false, false, 1>(v, &tw);
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < E; ++m) sub[t + (TQ + 1) * m] = v[0][m];
+      named_bar_sync(bar_id, GT);
+      if (p < TI) {
+        c32* dst = T + z * slice_stride + (long long)c * RB5;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n1 = p + TI * j;
+          const int word = n1 + n1 / TQ;
+          c32 w[5];
+          w[1] = tw5s[n1];
+          w[2] = cmul(w[1], w[1]);
+          w[3] = cmul(w[2], w[1]);
+          w[4] = cmul(w[2], w[2]);
+          c32 a[5];
+          a[0] = xb[word];
+#pragma unroll
+          for (int kk = 1; kk < 5; ++kk) a[kk] = cmulc(xb[kk * SW + word], w[kk]);
+          dft5<true>(a);
+#pragma unroll
+          for (int n2 = 0; n2 < 3; ++n2) {
+            const int n = n1 + Q * n2;
+            if (n < col_len) dst[(long long)(n >> 2) * rb_stride + (n & 3)] = a[n2];
+          }
+        }
+      }
+      mbar_arrive(empty);  // this thread's reads of xb are done
+      if (p == 0 && issued < nitems) {
+        mbar_wait(empty, (uint32_t)(item & 1));
+        issue();
+      }
+    }
+  }
+}
+
 // forward column FFT of full-length columns (PSF spectra): S[z][c][kx]
 template <int Q>
 __global__ void __launch_bounds__(Fft5Shape<Q>::T5)
@@ -270,11 +472,43 @@ int rows_inv5(const c32* T, float* out, const float* aux, int rows, int n_out, l
   return check_launch("k5_rows_inv");
 }
 
+#ifndef TF_K5_GROUPS
+#define TF_K5_GROUPS 3
+#endif
+template <bool FLIP>
+int cols_conv5_q1024(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices,
+                     cudaStream_t st) {
+  constexpr int Q = 1024, M = 5 * Q, G = TF_K5_GROUPS;
+  const int ncols = M / 2 + 1;
+  const int nrb = nrb5(col_len);
+  const int boxr = std::min(nrb, 256);
+  CUtensorMap map;
+  TF_TRY(encode_tmap(&map, T, M, nrb, nslices, boxr));
+  const size_t smem = (sizeof(c32) + sizeof(float)) * M + sizeof(c32) * G * 5 * (Q + Q / 32) +
+                      sizeof(c32) * Q + (2 * G + 1) * sizeof(uint64_t);
+  auto kern = k5_cols_conv_q1024<FLIP, G>;
+  TF_TRY(prep_kernel(kern, smem));
+  const int grid = std::max(1, std::min(ncols, num_sms()));
+  KernelTimer tm;
+  timer_begin(tm, 1, st);
+  kern<<<grid, G * 160, smem, st>>>(map, PQ, Bi, ncols, nrb, (int)nslices, boxr, T);
+  timer_end(tm);
+  return check_launch("k5_cols_conv_q1024");
+}
+
+#ifndef TF_K2_Q1024
+#define TF_K2_Q1024 1
+#endif
+
 template <int Q>
 int cols_conv5(c32* T, const c32* PQ, const float* Bi, int col_len, long long nslices, bool flip,
                cudaStream_t st) {
   using S = Fft5Shape<Q>;
   if (2 * col_len > S::M) return fail_arg("k5_cols_conv: column length %d exceeds M/2", col_len);
+  if constexpr (TF_K2_Q1024 && Q == 1024) {
+    return flip ? cols_conv5_q1024<true>(T, PQ, Bi, col_len, nslices, st)
+                : cols_conv5_q1024<false>(T, PQ, Bi, col_len, nslices, st);
+  }
   const size_t sm = smem5<Q>();
   auto kern = flip ? k5_cols_conv<Q, true> : k5_cols_conv<Q, false>;
   TF_TRY(prep_kernel(kern, sm));
