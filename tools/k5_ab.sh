@@ -7,6 +7,6 @@ echo "pytest rc=$?" >> gpurun_out/k5_tests.log
 out=gpurun_out/k5_ab.txt; : > $out
 for rep in 1 2; do
   for lib in paper_2603_28756_b200/libtomoforge_b200.so variants/lib_*.so; do
-    echo "$lib $(SWEEP_N=2560 SWEEP_SLICES=16 TF_LIB_PATH=$PWD/$lib timeout 300 python tools/toeplitz_sweep.py 2>&1 | tail -1)" >> $out
+    echo "$lib $(SWEEP_N=2560 SWEEP_SLICES=${K5_SLICES:-16} TF_LIB_PATH=$PWD/$lib timeout 300 python tools/toeplitz_sweep.py 2>&1 | tail -1)" >> $out
   done
 done
