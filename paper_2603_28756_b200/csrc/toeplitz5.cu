@@ -84,7 +84,8 @@ k5_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in
 template <int Q>
 __global__ void __launch_bounds__(Fft5Shape<Q>::T5)
 k5_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __restrict__ aux,
-            int rows, int n_out, long long os, long long orow, float alpha, float beta) {
+            int rows, int n_out, long long os, long long orow, float alpha, float beta,
+            int pf_dist) {
   using S = Fft5Shape<Q>;
   constexpr int M = S::M, H = M / 2 + 1, TP = S::TP;
   extern __shared__ __align__(16) c32 smem[];
@@ -92,6 +93,25 @@ k5_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __r
   const int z = blockIdx.y;
   const int u = blockIdx.x, r0 = 2 * u, rb = u >> 1, b0 = u & 1;
   const int nrb = nrb5(rows);
+  // L2 prefetch of the row block (both row pairs) and aux rows of the CTA pf_dist
+  // blocks ahead, as K3 of the power-of-two path: the loads below are latency-bound
+  // (long-scoreboard stalls) otherwise
+  if (pf_dist > 0 && p == 32) {
+    const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + pf_dist;
+    if (lin < (long long)gridDim.x * gridDim.y) {
+      const int zz = (int)(lin / gridDim.x), uu = (int)(lin - (long long)zz * gridDim.x);
+      if ((uu & 1) == 0) {
+        bulk_prefetch_l2(T + ((long long)zz * nrb + (uu >> 1)) * H * RB5,
+                         (uint32_t)(H * RB5 * sizeof(c32)));
+      }
+      if (aux && (n_out * sizeof(float)) % 16 == 0 && (orow * sizeof(float)) % 16 == 0 &&
+          (os * sizeof(float)) % 16 == 0 && reinterpret_cast<uintptr_t>(aux) % 16 == 0) {
+        for (int q = 0; q < 2 && 2 * uu + q < rows; ++q)
+          bulk_prefetch_l2(aux + zz * os + (long long)(2 * uu + q) * orow,
+                           (uint32_t)(n_out * sizeof(float)));
+      }
+    }
+  }
   const float4* src = reinterpret_cast<const float4*>(T + ((long long)z * nrb + rb) * H * RB5);
   const int g = p / TP, t = p - g * TP;
   // the row pair's half spectrum (Ya, Yb)(k), k <= M/2: coalesced loads into shared
@@ -452,6 +472,10 @@ int rows_fwd5(const float* x, c32* T, int rows, int n_in, long long xs, long lon
   return check_launch("k5_rows_fwd");
 }
 
+// L2 prefetch distance of k5_rows_inv in multiples of the SM count (0 = off)
+#ifndef TF_K5_PF_MUL
+#define TF_K5_PF_MUL 1
+#endif
 template <int Q>
 int rows_inv5(const c32* T, float* out, const float* aux, int rows, int n_out, long long os,
               long long orow, float alpha, float beta, long long nslices, cudaStream_t st) {
@@ -466,7 +490,8 @@ int rows_inv5(const c32* T, float* out, const float* aux, int rows, int n_out, l
     const int nz = (int)std::min<long long>(65535, nslices - z0);
     k5_rows_inv<Q><<<dim3(units, nz), S::T5, sm, st>>>(
         T + z0 * (long long)(S::M / 2 + 1) * RB5 * nrb5(rows), out + z0 * os,
-        aux ? aux + z0 * os : nullptr, rows, n_out, os, orow, alpha, beta);
+        aux ? aux + z0 * os : nullptr, rows, n_out, os, orow, alpha, beta,
+        TF_K5_PF_MUL * num_sms());
   }
   timer_end(tm);
   return check_launch("k5_rows_inv");
