@@ -14,8 +14,10 @@ SWEEP_SLICES=64 timeout 900 ncu $F -k regex:'k_rows_fwd_pf|k_cols_conv64|k_rows_
 SWEEP_N=2560 SWEEP_SLICES=16 timeout 900 ncu $F -k regex:'k5_rows|k5_cols_conv' -s 12 -c 3 \
   -o gpurun_out/prof_toeplitz5_$TAG -f python tools/toeplitz_sweep.py > /dev/null 2>&1
 # solver kernels (64 x 2048^2)
-timeout 900 ncu $F -k regex:'k_prior_update_sym|k_energy_fid_t|k_prior_energy_update' -s 3 -c 3 \
+timeout 900 ncu $F -k regex:'k_prior_update_sym|k_energy_fid_t' -s 1 -c 2 \
   -o gpurun_out/prof_solver_$TAG -f python tools/solver_probe.py > /dev/null 2>&1
+timeout 900 ncu $F -k regex:'k_prior_energy_update' -s 1 -c 1 \
+  -o gpurun_out/prof_k45_$TAG -f python tools/solver_probe.py > /dev/null 2>&1
 # one-time kernels (8 x 2048^2)
 PROBE_SLICES=8 timeout 900 ncu $F -k regex:'k_spread|k_nufft_rows|k_nufft_cols|k_detector_rows|k_upsample3' \
   -c 6 -o gpurun_out/prof_onetime_$TAG -f python tools/nufft_probe.py > /dev/null 2>&1
