@@ -26,12 +26,16 @@ def _sanitizer():
 
 
 # N = 128 runs the generic kernels; N = 512 the TMA / bulk-copy / 256-bit paths and
-# interior K4/K5 tiles; N = 1024 "toeplitz" the radix-64 column kernel (M = 2048)
+# interior K4/K5 tiles; N = 1024 "toeplitz" the radix-64 column kernel (M = 2048), N = 2560
+# the radix-5 column kernel of M = 5120
 @pytest.mark.parametrize("tool,n,mode", [("memcheck", 128, ""), ("memcheck", 512, ""),
                                          ("racecheck", 128, ""), ("racecheck", 512, ""),
                                          ("synccheck", 512, ""), ("memcheck", 1024, "toeplitz"),
                                          ("racecheck", 1024, "toeplitz"),
-                                         ("synccheck", 1024, "toeplitz")])
+                                         ("synccheck", 1024, "toeplitz"),
+                                         ("memcheck", 2560, "toeplitz"),
+                                         ("racecheck", 2560, "toeplitz"),
+                                         ("synccheck", 2560, "toeplitz")])
 def test_kernels_clean_under_sanitizer(tool, n, mode):
     import torch
 
