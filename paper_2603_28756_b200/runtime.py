@@ -52,6 +52,8 @@ __all__ = [
     "exchange_halos",
     "distributed_solve",
     "distributed_solve_hierarchical",
+    "InProcessTransport",
+    "SocketTransport",
 ]
 
 
@@ -68,6 +70,33 @@ class TransportTimeout(TransportError):
 
 
 @dataclass(frozen=True)
+class _TransportMarker:
+    """Name-compatible stand-in for the reference's CPU transports (runtime.py:190-286).
+
+    The reference models MPI with in-process queues or local sockets between worker
+    threads; here the slab workers are GPU processes and the transport is the
+    torch.distributed group (NCCL, or gloo for tests), plus optional peer-memory
+    halos (``halo="peer"``).  Instances are accepted wherever the reference takes a
+    ``transport`` argument and are otherwise inert: the queue / socket protocol itself
+    is out of scope."""
+
+    def __init__(self, n_workers: int, *args, **kwargs):
+        if n_workers < 1:
+            raise ValueError("need at least one worker")
+        self.n_workers = n_workers
+
+    def close(self):
+        pass
+
+
+class InProcessTransport(_TransportMarker):
+    __doc__ = _TransportMarker.__doc__
+
+
+class SocketTransport(_TransportMarker):
+    __doc__ = _TransportMarker.__doc__
+
+
 class SlabPartition:
     """Contiguous slice range [begin, end) owned by one worker (runtime.py:82-105)."""
 

@@ -82,3 +82,16 @@ def test_slab_comm_gloo(tmp_path, world, n_slices):
     total = sum(np.load(tmp_path / f"rank{p.worker_id}.npy", allow_pickle=True).item()["halo_msgs"]
                 for p in parts)
     assert total == 2 * (world - 1)
+
+
+def test_reference_transport_names_are_accepted():
+    """InProcessTransport / SocketTransport exist for drop-in imports and are accepted
+    (and ignored) where the reference takes a transport (runtime.py:190-286)."""
+    import paper_2603_28756_b200 as tf
+
+    for cls in (tf.InProcessTransport, tf.SocketTransport):
+        t = cls(2)
+        assert t.n_workers == 2
+        t.close()
+    with pytest.raises(ValueError):
+        tf.InProcessTransport(0)
