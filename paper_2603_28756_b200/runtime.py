@@ -69,7 +69,6 @@ class TransportTimeout(TransportError):
     """An expected neighbour message never arrived (collective timeout)."""
 
 
-@dataclass(frozen=True)
 class _TransportMarker:
     """Name-compatible stand-in for the reference's CPU transports (runtime.py:190-286).
 
@@ -97,6 +96,7 @@ class SocketTransport(_TransportMarker):
     __doc__ = _TransportMarker.__doc__
 
 
+@dataclass(frozen=True)
 class SlabPartition:
     """Contiguous slice range [begin, end) owned by one worker (runtime.py:82-105)."""
 
