@@ -318,6 +318,32 @@ __device__ __forceinline__ void fftn(c32 (&v)[NB][E], c32* sm, int sbs, int t,
   fft_passes_from<M, E, 0, INV, ZIN, HOUT, NB, PP>(v, sm, sbs, t, twf);
 }
 
+// Forward passes 0 .. NP-2 of fftn (no ping-pong), ending with pass NP-2's outputs
+// stored in the exchange buffer and a barrier.  The caller loads the last pass's
+// inputs in a thread mapping of its own (any canonical columns t, via canon_word)
+// and runs the last pass itself with fft_pass<M, E, NP-1, ...> -- e.g. so that one
+// thread holds both halves of a Hermitian mirror pair (k_rows_fwd_pf).
+template <int M, int E, int P, bool ZIN, int NB>
+__device__ __forceinline__ void fftn_to_last(c32 (&v)[NB][E], c32* sm, int sbs, int t,
+                                             const PassTw<M, E, P>* tw = nullptr) {
+  using S = FftShape<M, E>;
+  static_assert(S::NP >= 2 && P + 1 < S::NP, "needs a last exchange");
+  if constexpr (P > 0) fft_pass<M, E, P, false, false, false, NB>(v, tw);
+  else fft_pass<M, E, 0, false, ZIN, false, NB>(v, (const PassTw<M, E, 0>*)nullptr);
+  if constexpr (P + 2 < S::NP) {
+    PassTw<M, E, P + 1> next;
+    next.from_table(t);
+    fft_store<M, E, P, NB>(v, sm, sbs, t);
+    __syncthreads();
+    load_canonical<M, E, NB>(v, sm, sbs, t);
+    __syncthreads();
+    fftn_to_last<M, E, P + 1, ZIN, NB>(v, sm, sbs, t, &next);
+  } else {
+    fft_store<M, E, P, NB>(v, sm, sbs, t);
+    __syncthreads();
+  }
+}
+
 // single transform
 template <int M, int E, bool INV, bool ZIN = false, bool HOUT = false>
 __device__ __forceinline__ void fft(c32 (&v)[E], c32* sm, int t) {

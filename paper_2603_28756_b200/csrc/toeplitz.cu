@@ -121,12 +121,22 @@ k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
   if (t == 0) emit(M / 2, E / 2, true);
 }
 
+#ifndef TF_K1_MIRROR
+#define TF_K1_MIRROR 1
+#endif
+#ifndef TF_K3_MIRROR
+#define TF_K3_MIRROR 1
+#endif
 // Persistent K1 with a bulk-copied input stage.  Each CTA walks units u =
 // blockIdx.x + i * gridDim.x (unit = (slice, 4-row block)); the four input rows
 // of the next unit are fetched by the copy engine (cp.async.bulk, one 1-D copy
 // per row) into the single shared stage as soon as the current unit has read
 // it, so the load latency overlaps this unit's FFT.  Needs 16-byte aligned rows
 // of n_in * 4 bytes.  Same transform and output as k_rows_fwd (NB = 2).
+// TF_K1_MIRROR (default): the last pass runs in a mirror-pair mapping (thread
+// t = 2s + b owns columns s and T - s of row pair b), so Z(k) and Z(M - k) meet
+// in registers and the Hermitian split needs no shared-memory round trip; lane
+// pairs b = 0, 1 write the two 16-byte halves of each 32-byte output word.
 template <int M, int E, bool ZP>
 __global__ void __launch_bounds__(M / E, (M >= 8192 ? 1 : 2))
 k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
@@ -141,6 +151,16 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
   float* stage = reinterpret_cast<float*>(smem + NB * SB);          // [RB][n_in]
   uint64_t* full = reinterpret_cast<uint64_t*>(stage + RB * n_in);  // 8-byte aligned
   const int t = threadIdx.x;
+  using S = FftShape<M, E>;
+  constexpr bool MIR = TF_K1_MIRROR && TT % 32 == 0 && S::NP >= 2;
+  const int mb = t & 1, s = t >> 1;  // transform (row pair) and mirror slot
+  const bool s0 = s == 0;
+  const int c1 = s, c2 = s0 ? TT / 2 : TT - s;
+  PassTw<M, E, S::NP - 1> tw1, tw2;  // last-pass twiddles of the thread's two columns
+  if constexpr (MIR) {
+    tw1.from_table(c1);
+    tw2.from_table(c2);
+  }
   const int nrb = nrb_of(rows);
   const uint32_t row_bytes = (uint32_t)n_in * sizeof(float);
   // (slice, row block) walks of the consumer and of the producer (one unit ahead),
@@ -194,31 +214,61 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
       fence_proxy_async_smem();
       issue();
     }
-    fftn<M, E, false, ZP, false, NB>(v, sm, SB, t);
+    if constexpr (MIR) {
+      fftn_to_last<M, E, 0, ZP, NB>(v, sm, SB, t);
+      // last pass in the mirror-pair mapping: thread t = 2s + b takes columns c1 = s,
+      // c2 = T - s (s = 0: 0 and T/2) of transform b, so Z(k) and Z(M - k) are both in
+      // its registers and the split needs no shared-memory round trip
+      {
+        c32 w[2][1][E];
 #pragma unroll
-    for (int m = E / 2; m < E; ++m)
+        for (int m = 0; m < E; ++m) {
+          w[0][0][m] = sm[mb * SB + canon_word<M, E>(c1, m)];
+          w[1][0][m] = sm[mb * SB + canon_word<M, E>(c2, m)];
+        }
+        fft_pass<M, E, S::NP - 1, false, false, false, 1>(w[0], &tw1);
+        fft_pass<M, E, S::NP - 1, false, false, false, 1>(w[1], &tw2);
+        float4* dst = reinterpret_cast<float4*>(T + ((long long)z * nrb + rb) * H * RB) + mb;
+        auto split = [](c32 zk, c32 zm) {
+          return make_float4(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y), 0.5f * (zk.y + zm.y),
+                             0.5f * (zm.x - zk.x));
+        };
 #pragma unroll
-      for (int b = 0; b < NB; ++b) sm[b * SB + t + TT * m - M / 2] = v[b][m];
-    __syncthreads();
-    float4* dst = reinterpret_cast<float4*>(T + ((long long)z * nrb + rb) * H * RB);
-    auto emit = [&](int k, int m, bool self) {
-      float4 o[NB];
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const c32 zk = v[b][m];
-        const c32 zm = self ? zk : sm[b * SB + M / 2 - k];
-        const c32 xa = scale(mk(zk.x + zm.x, zk.y - zm.y), 0.5f);
-        const c32 xb = scale(mk(zk.y + zm.y, zm.x - zk.x), 0.5f);
-        o[b] = make_float4(xa.x, xa.y, xb.x, xb.y);
+        for (int m = 0; m < E / 2; ++m) {
+          const c32 m1 = s0 ? w[0][0][(E - m) % E] : w[1][0][E - 1 - m];
+          const c32 m2 = s0 ? w[1][0][E - 1 - m] : w[0][0][E - 1 - m];
+          dst[2 * (c1 + TT * m)] = split(w[0][0][m], m1);
+          dst[2 * (c2 + TT * m)] = split(w[1][0][m], m2);
+        }
+        if (s0) dst[2 * (M / 2)] = split(w[0][0][E / 2], w[0][0][E / 2]);
       }
-      st_global_v8(dst + 2 * k, o[0], o[1]);
-    };
+    } else {
+      fftn<M, E, false, ZP, false, NB>(v, sm, SB, t);
 #pragma unroll
-    for (int m = 0; m < E / 2; ++m) {
-      const int k = t + TT * m;
-      emit(k, m, k == 0);
+      for (int m = E / 2; m < E; ++m)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) sm[b * SB + t + TT * m - M / 2] = v[b][m];
+      __syncthreads();
+      float4* dst = reinterpret_cast<float4*>(T + ((long long)z * nrb + rb) * H * RB);
+      auto emit = [&](int k, int m, bool self) {
+        float4 o[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const c32 zk = v[b][m];
+          const c32 zm = self ? zk : sm[b * SB + M / 2 - k];
+          const c32 xa = scale(mk(zk.x + zm.x, zk.y - zm.y), 0.5f);
+          const c32 xb = scale(mk(zk.y + zm.y, zm.x - zk.x), 0.5f);
+          o[b] = make_float4(xa.x, xa.y, xb.x, xb.y);
+        }
+        st_global_v8(dst + 2 * k, o[0], o[1]);
+      };
+#pragma unroll
+      for (int m = 0; m < E / 2; ++m) {
+        const int k = t + TT * m;
+        emit(k, m, k == 0);
+      }
+      if (t == 0) emit(M / 2, E / 2, true);
     }
-    if (t == 0) emit(M / 2, E / 2, true);
     // the next unit's pass-0 exchange store must not overtake the mirror reads:
     // its first shared write follows the stage barrier above, which every
     // thread reaches only after finishing this unit
@@ -230,8 +280,11 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
 // out[n] = alpha * y[n] + beta * aux[n] for n < n_out (n_out <= M/2).
 // Thread t of group g inverts block rb's two row pairs with complex FFTs of
 // Z = Y_a + i Y_b (Hermitian extension Z(j) = conj Y_a(M-j) + i conj Y_b(M-j)
-// for j > M/2).  It loads the 32 contiguous bytes of its own k = t + T m
-// (m < E/2); the mirrored half comes from partner thread T-t via shared memory.
+// for j > M/2).  TF_K3_MIRROR (default): thread t = 2s + b loads the 16-byte
+// (Ya, Yb) words of columns s and T - s of row pair b -- each other's Hermitian
+// mirrors -- and runs the first pass on both before the first exchange.  Otherwise
+// it loads the 32 contiguous bytes of its own k = t + T m (m < E/2) and the
+// mirrored half comes from partner thread T-t via shared memory.
 // AUXBULK: the four aux rows are prefetched into shared memory by 1-D bulk
 // copies issued at kernel start (needs 16-byte aligned rows of n_out*4 bytes).
 template <int M, int E, int G, bool AUXBULK, int NB>
@@ -307,46 +360,93 @@ k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __re
   auto fix = [&](int k, float4& y) {
     if (k == 0 || k == M / 2) { y.y = 0.f; y.w = 0.f; }  // irfft drops Im(DC, Nyquist)
   };
-  float4 lo[E / 2][NB];
-#pragma unroll
-  for (int m = 0; m < E / 2; ++m) {
-    if constexpr (NB == 2) ld_global_nc_v8(src + 2 * (t + TT * m), lo[m][0], lo[m][NB - 1]);
-    else lo[m][0] = __ldg(src + 2 * (t + TT * m) + b0);
-  }
-  float4 nyq[NB];
-  if (t == 0)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) nyq[b] = __ldg(src + 2 * (M / 2) + b + b0);
-#pragma unroll
-  for (int m = 0; m < E / 2; ++m)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      fix(t + TT * m, lo[m][b]);
-      *reinterpret_cast<float4*>(sm + b * SB + 2 * (t + TT * m)) = lo[m][b];
-    }
-  if (t == 0)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      fix(M / 2, nyq[b]);
-      *reinterpret_cast<float4*>(sm + b * SB + 2 * (M / 2)) = nyq[b];
-    }
-  __syncthreads();
+  using S = FftShape<M, E>;
+  constexpr bool MIR = TF_K3_MIRROR && NB == 2 && TT % 32 == 0 && S::NP >= 2;
   c32 v[NB][E];
+  if constexpr (MIR) {
+    // first pass in the mirror-pair mapping (as in k_rows_fwd_pf): thread t = 2s + b
+    // loads the 16-byte (Ya, Yb) words of columns c1 = s and c2 = T - s (s = 0: 0 and
+    // T/2) of row pair b, which hold each other's Hermitian mirrors, runs pass 0 on
+    // both and stores them to the first exchange -- no mirror round trip
+    const int mb = t & 1, s = t >> 1;
+    const bool s0 = s == 0;
+    const int c1 = s, c2 = s0 ? TT / 2 : TT - s;
+    const float4* sb = src + mb;
+    float4 y1[E / 2], y2[E / 2], yn;
 #pragma unroll
-  for (int m = 0; m < E; ++m)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      if (m < E / 2) {
-        const float4 y = lo[m][b];
-        v[b][m] = mk(y.x - y.w, y.y + y.z);  // Ya + i Yb
-      } else {
-        const int j = t + TT * m;
-        const float4 y = *reinterpret_cast<const float4*>(sm + b * SB + 2 * (M - j));
-        v[b][m] = mk(y.x + y.w, y.z - y.y);  // conj(Ya) + i conj(Yb)
-      }
+    for (int m = 0; m < E / 2; ++m) {
+      y1[m] = __ldg(sb + 2 * (c1 + TT * m));
+      y2[m] = __ldg(sb + 2 * (c2 + TT * m));
     }
-  __syncthreads();
-  fftn<M, E, true, false, true, NB>(v, sm, SB, t);
+    if (s0) {
+      yn = __ldg(sb + 2 * (M / 2));
+      fix(0, y1[0]);
+      fix(M / 2, yn);
+    }
+    PassTw<M, E, 1> tw;
+    tw.from_table(t);
+    c32 w[2][1][E];
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+      w[0][0][m] = mk(y1[m].x - y1[m].w, y1[m].y + y1[m].z);  // Ya + i Yb
+      w[1][0][m] = mk(y2[m].x - y2[m].w, y2[m].y + y2[m].z);
+    }
+#pragma unroll
+    for (int m = E / 2; m < E; ++m) {  // conj(Ya) + i conj(Yb) at M - j
+      const float4 a = s0 ? (m == E / 2 ? yn : y1[E - m]) : y2[E - 1 - m];
+      const float4 c = s0 ? y2[E - 1 - m] : y1[E - 1 - m];
+      w[0][0][m] = mk(a.x + a.w, a.z - a.y);
+      w[1][0][m] = mk(c.x + c.w, c.z - c.y);
+    }
+    fft_pass<M, E, 0, true, false, false, 1>(w[0], (const PassTw<M, E, 0>*)nullptr);
+    fft_pass<M, E, 0, true, false, false, 1>(w[1], (const PassTw<M, E, 0>*)nullptr);
+    fft_store<M, E, 0, 1>(w[0], sm + mb * SB, SB, c1);
+    fft_store<M, E, 0, 1>(w[1], sm + mb * SB, SB, c2);
+    __syncthreads();
+    load_canonical<M, E, NB>(v, sm, SB, t);
+    __syncthreads();
+    fft_passes_from<M, E, 1, true, false, true, NB, false>(v, sm, SB, t, TwTable(), &tw);
+  } else {
+    float4 lo[E / 2][NB];
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+      if constexpr (NB == 2) ld_global_nc_v8(src + 2 * (t + TT * m), lo[m][0], lo[m][NB - 1]);
+      else lo[m][0] = __ldg(src + 2 * (t + TT * m) + b0);
+    }
+    float4 nyq[NB];
+    if (t == 0)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) nyq[b] = __ldg(src + 2 * (M / 2) + b + b0);
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        fix(t + TT * m, lo[m][b]);
+        *reinterpret_cast<float4*>(sm + b * SB + 2 * (t + TT * m)) = lo[m][b];
+      }
+    if (t == 0)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        fix(M / 2, nyq[b]);
+        *reinterpret_cast<float4*>(sm + b * SB + 2 * (M / 2)) = nyq[b];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (m < E / 2) {
+          const float4 y = lo[m][b];
+          v[b][m] = mk(y.x - y.w, y.y + y.z);  // Ya + i Yb
+        } else {
+          const int j = t + TT * m;
+          const float4 y = *reinterpret_cast<const float4*>(sm + b * SB + 2 * (M - j));
+          v[b][m] = mk(y.x + y.w, y.z - y.y);  // conj(Ya) + i conj(Yb)
+        }
+      }
+    __syncthreads();
+    fftn<M, E, true, false, true, NB>(v, sm, SB, t);
+  }
   if constexpr (AUXBULK) mbar_wait(abar, 0);
   if (!writer) return;
 
