@@ -141,6 +141,22 @@ def test_apply_2048_vs_oracle(tf, nd):
     assert rel_l2(out, ref) < 1e-5
 
 
+@pytest.mark.parametrize("nd", [2900])
+def test_apply_8192_vs_oracle(tf, nd):
+    """M = 8192 (2560 < N <= 4096): four-pass row transforms, so the mirror-pair
+    last pass of K1 and first pass of K3 run after / before two exchanges."""
+    import oracle as O
+
+    n = 2900
+    ang = np.linspace(0, np.pi, 16, endpoint=False)
+    x = np.random.default_rng(3).standard_normal((1, n, n))
+    ref = O.apply_batch(O.build_psf(ang, nd, n), x)
+    psf = _psf(tf, ang, nd, n)
+    assert psf.fft_side == 8192
+    out = tf.toeplitz_apply(psf, x)
+    assert rel_l2(out, ref) < 1e-5
+
+
 def test_device_tensor_path(tf):
     import torch
 
