@@ -127,6 +127,11 @@ k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
 #ifndef TF_K3_MIRROR
 #define TF_K3_MIRROR 1
 #endif
+// K1 (mirror path): the split outputs are staged in the freed exchange buffer and
+// written by one bulk async copy per row block instead of per-thread stores
+#ifndef TF_K1_BULKST
+#define TF_K1_BULKST 1
+#endif
 // Persistent K1 with a bulk-copied input stage.  Each CTA walks units u =
 // blockIdx.x + i * gridDim.x (unit = (slice, 4-row block)); the four input rows
 // of the next unit are fetched by the copy engine (cp.async.bulk, one 1-D copy
@@ -137,6 +142,10 @@ k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
 // t = 2s + b owns columns s and T - s of row pair b), so Z(k) and Z(M - k) meet
 // in registers and the Hermitian split needs no shared-memory round trip; lane
 // pairs b = 0, 1 write the two 16-byte halves of each 32-byte output word.
+// TF_K1_BULKST (default): those words go to the (by then free) exchange buffer
+// in the block's HBM layout, and one bulk async copy writes the 64 KB block --
+// the LSU issues 16 shared stores per thread instead of 16 global ones, and the
+// copy overlaps the next unit (K1 0.68 -> 0.62 ms).
 template <int M, int E, bool ZP>
 __global__ void __launch_bounds__(M / E, (M >= 8192 ? 1 : 2))
 k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
@@ -209,6 +218,9 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
         v[b][m] = mk(a, c);
       }
     }
+    if constexpr (MIR && TF_K1_BULKST) {
+      if (t == 0) bulk_wait_read<0>();  // the previous unit's output copy has left sm
+    }
     __syncthreads();  // the stage is free: refill it with the next unit
     if (t == 0 && u + gridDim.x < nunits) {
       fence_proxy_async_smem();
@@ -228,7 +240,12 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
         }
         fft_pass<M, E, S::NP - 1, false, false, false, 1>(w[0], &tw1);
         fft_pass<M, E, S::NP - 1, false, false, false, 1>(w[1], &tw2);
-        float4* dst = reinterpret_cast<float4*>(T + ((long long)z * nrb + rb) * H * RB) + mb;
+        float4* blk = reinterpret_cast<float4*>(T + ((long long)z * nrb + rb) * H * RB);
+        float4* dst = blk + mb;
+        if constexpr (TF_K1_BULKST) {
+          __syncthreads();  // every thread's last-pass loads are done: sm is free
+          dst = reinterpret_cast<float4*>(sm) + mb;
+        }
         auto split = [](c32 zk, c32 zm) {
           return make_float4(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y), 0.5f * (zk.y + zm.y),
                              0.5f * (zm.x - zk.x));
@@ -241,6 +258,15 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
           dst[2 * (c2 + TT * m)] = split(w[1][0][m], m2);
         }
         if (s0) dst[2 * (M / 2)] = split(w[0][0][E / 2], w[0][0][E / 2]);
+        if constexpr (TF_K1_BULKST) {
+          static_assert(!TF_K1_BULKST || H * RB <= NB * SB, "output block fits the exchange");
+          fence_proxy_async_smem();
+          __syncthreads();
+          if (t == 0) {
+            bulk_s2g(blk, sm, (uint32_t)(H * RB * sizeof(c32)));
+            bulk_commit();
+          }
+        }
       }
     } else {
       fftn<M, E, false, ZP, false, NB>(v, sm, SB, t);
@@ -272,6 +298,9 @@ k_rows_fwd_pf(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_
     // the next unit's pass-0 exchange store must not overtake the mirror reads:
     // its first shared write follows the stage barrier above, which every
     // thread reaches only after finishing this unit
+  }
+  if constexpr (MIR && TF_K1_BULKST) {
+    if (t == 0) bulk_wait<0>();  // the last output copy is complete before the CTA exits
   }
 }
 
