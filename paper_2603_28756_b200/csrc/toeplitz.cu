@@ -132,6 +132,10 @@ k_rows_fwd(const float* __restrict__ x, c32* __restrict__ T, int rows, int n_in,
 #ifndef TF_K1_BULKST
 #define TF_K1_BULKST 1
 #endif
+// K3: output rows staged in the freed exchange buffer, one bulk async copy per row
+#ifndef TF_K3_BULKST
+#define TF_K3_BULKST 1
+#endif
 // Persistent K1 with a bulk-copied input stage.  Each CTA walks units u =
 // blockIdx.x + i * gridDim.x (unit = (slice, 4-row block)); the four input rows
 // of the next unit are fetched by the copy engine (cp.async.bulk, one 1-D copy
@@ -320,7 +324,7 @@ template <int M, int E, int G, bool AUXBULK, int NB>
 __global__ void __launch_bounds__(G*(M / E), (M >= 8192 ? 1 : 2))
 k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __restrict__ aux,
            int rows, int n_out, long long o_slice_stride, long long o_row_stride, float alpha,
-           float beta, int pf_dist) {
+           float beta, int pf_dist, int obulk) {
   constexpr int TT = M / E;
   constexpr int H = M / 2 + 1;
   constexpr int SB = group_stride(M, NB * G);
@@ -478,6 +482,37 @@ k_rows_inv(const c32* __restrict__ T, float* __restrict__ out, const float* __re
   }
   if constexpr (AUXBULK) mbar_wait(abar, 0);
   if (!writer) return;
+  if constexpr (TF_K3_BULKST && G == 1 && NB == 2) {
+    if (obulk) {  // 16-byte aligned output rows: stage them, one bulk copy per row
+      static_assert(NR * (M / 2) * sizeof(float) <= NB * SB * sizeof(c32), "rows fit");
+      float* so = reinterpret_cast<float*>(sm);
+      __syncthreads();  // every thread's last exchange reads are done: sm is free
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const float* a = aux ? aux + zo + (long long)(r0 + q) * o_row_stride : nullptr;
+#pragma unroll
+        for (int m = 0; m < E / 2; ++m) {
+          const int n = t + TT * m;
+          if (n < n_out) {
+            float y = alpha * ((q & 1) ? v[q >> 1][m].y : v[q >> 1][m].x);
+            if constexpr (AUXBULK) y = fmaf(beta, auxs[q * (M / 2) + n], y);
+            else if (a && r0 + q < rows) y = fmaf(beta, __ldg(a + n), y);
+            so[q * (M / 2) + n] = y;
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (t == 0) {
+        for (int q = 0; q < NR && r0 + q < rows; ++q)
+          bulk_s2g(out + zo + (long long)(r0 + q) * o_row_stride, so + q * (M / 2),
+                   (uint32_t)n_out * sizeof(float));
+        bulk_commit();
+        bulk_wait_read<0>();  // the staged rows have left shared memory
+      }
+      return;
+    }
+  }
 
 #pragma unroll
   for (int q = 0; q < NR; ++q) {
@@ -1064,6 +1099,8 @@ int launch_rows_inv_t(const c32* T, float* out, const float* aux, int rows, int 
   // bulk-prefetch aux rows when they are 16-byte aligned blocks
   const bool bulk = aux && (n_out % 4 == 0) && (orow % 4 == 0) && (os % 4 == 0) &&
                     (reinterpret_cast<uintptr_t>(aux) % 16 == 0);
+  const int obulk = (n_out % 4 == 0) && (orow % 4 == 0) && (os % 4 == 0) &&
+                    (reinterpret_cast<uintptr_t>(out) % 16 == 0);
   const size_t smem = sizeof(c32) * NB * G * group_stride(M, NB * G) +
                       (bulk ? sizeof(float) * G * 2 * NB * (M / 2) + 16 : 0);
   auto kern = bulk ? k_rows_inv<M, E, G, true, NB> : k_rows_inv<M, E, G, false, NB>;
@@ -1076,7 +1113,7 @@ int launch_rows_inv_t(const c32* T, float* out, const float* aux, int rows, int 
     const int nz = (int)std::min<long long>(65535, nslices - z0);
     kern<<<dim3(gx, nz), G * TT, smem, st>>>(T + z0 * (long long)(M / 2 + 1) * RB * nrb_of(rows),
                                              out + z0 * os, aux ? aux + z0 * os : nullptr, rows,
-                                             n_out, os, orow, alpha, beta, k3_l2pf());
+                                             n_out, os, orow, alpha, beta, k3_l2pf(), obulk);
   }
   timer_end(tm);
   return check_launch("k_rows_inv");
