@@ -181,7 +181,10 @@ def test_repeated_apply_bitwise_stable(tf):
 
 
 @pytest.mark.parametrize("n,nd,z", [(700, 700, 1), (700, 701, 2), (1000, 1024, 5),
-                                    (1400, 1400, 3), (1400, 1401, 6)])
+                                    (1400, 1400, 3), (1400, 1401, 6),
+                                    # N % 4 != 0: partial last row block, per-thread
+                                    # row stores instead of the bulk paths
+                                    (1001, 1001, 2), (1022, 1024, 1)])
 def test_apply_radix64_columns_vs_oracle(tf, n, nd, z):
     """The two-pass radix-64 column kernel (k_cols_conv64: M = 2048 for 640 < N <= 1024,
     M = 4096 for 1280 < N <= 2048): slice counts that leave some of its four
