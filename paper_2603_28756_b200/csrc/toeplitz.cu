@@ -1087,7 +1087,10 @@ int launch_rows_fwd(const float* x, c32* T, int rows, int n_in, long long xs, lo
 // How many blocks ahead a K3 CTA prefetches the spectrum block and aux rows into
 // L2: one per SM, about half a resident wave ahead.  Measured on 64 x 2048^2:
 // 0.92 -> 0.78 ms (110-200 equal, 592 thrashes).
-inline int k3_l2pf() { return num_sms(); }
+#ifndef TF_K3_PF_X2
+#define TF_K3_PF_X2 2  // K3 L2 prefetch distance in half SM counts
+#endif
+inline int k3_l2pf() { return num_sms() * TF_K3_PF_X2 / 2; }
 
 template <int M, int NB>
 int launch_rows_inv_t(const c32* T, float* out, const float* aux, int rows, int n_out,
