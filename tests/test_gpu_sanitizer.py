@@ -26,13 +26,17 @@ def _sanitizer():
 
 
 # N = 128 runs the generic kernels; N = 512 the TMA / bulk-copy / 256-bit paths and
-# interior K4/K5 tiles; N = 1024 "toeplitz" the radix-64 column kernel (M = 2048), N = 2560
+# interior K4/K5 tiles; N = 1024 "toeplitz" the radix-64 column kernel (M = 2048), N = 2048
+# the M = 4096 chain (K1 mirror pass + bulk block copies, K3 bulk row copies), N = 2560
 # the radix-5 column kernel of M = 5120
 @pytest.mark.parametrize("tool,n,mode", [("memcheck", 128, ""), ("memcheck", 512, ""),
                                          ("racecheck", 128, ""), ("racecheck", 512, ""),
                                          ("synccheck", 512, ""), ("memcheck", 1024, "toeplitz"),
                                          ("racecheck", 1024, "toeplitz"),
                                          ("synccheck", 1024, "toeplitz"),
+                                         ("memcheck", 2048, "toeplitz"),
+                                         ("racecheck", 2048, "toeplitz"),
+                                         ("synccheck", 2048, "toeplitz"),
                                          ("memcheck", 2560, "toeplitz"),
                                          ("racecheck", 2560, "toeplitz"),
                                          ("synccheck", 2560, "toeplitz")])
