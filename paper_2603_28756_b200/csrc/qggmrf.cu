@@ -752,8 +752,11 @@ k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const floa
 // fp64 arithmetic, so when iteration k does not restart the result is the one
 // the unfused K5 -> decide -> K4 sequence gives; after a restart the solver
 // re-runs K4 with c = 0 (k_prior_update_sym with `only_if` = the restart flag).
+#ifndef TF_K45_MINB
+#define TF_K45_MINB 3  // 3 CTAs (24 warps) per SM at 80 registers: 5.33 -> 5.22 ms despite small spills
+#endif
 template <bool P2, bool NONNEG>
-__global__ void __launch_bounds__(TX* TY, 2)
+__global__ void __launch_bounds__(TX* TY, TF_K45_MINB)
 k_prior_energy_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* Kfp,
                       const float* __restrict__ rstar, float* f_new, double* __restrict__ partial,
                       int nz, int h, int w, float lam, float inv_L, int energy, PriorConsts pc,
