@@ -320,6 +320,9 @@ k_prior_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* K
 // the same choice (its update must equal K4's bit for bit), and K45's XU also
 // carries the energy's transcendentals: 6 is best for K45 (measured on 64 x 2048^2:
 // K45 5.36 ms at 3, 5.32 at 6, 5.35 with none; K4 alone 3.15 / 3.17 / 3.20)
+#ifndef TF_K45_MB3
+#define TF_K45_MB3 1  // allow the 3-CTA K45 when the wave count favours it
+#endif
 #ifndef TF_XRCP_K4
 #define TF_XRCP_K4 6
 #endif
@@ -752,11 +755,12 @@ k_prior_update_sym(Planes F, Planes FP, const float* __restrict__ Kf, const floa
 // fp64 arithmetic, so when iteration k does not restart the result is the one
 // the unfused K5 -> decide -> K4 sequence gives; after a restart the solver
 // re-runs K4 with c = 0 (k_prior_update_sym with `only_if` = the restart flag).
-#ifndef TF_K45_MINB
-#define TF_K45_MINB 3  // 3 CTAs (24 warps) per SM at 80 registers: 5.33 -> 5.22 ms despite small spills
-#endif
-template <bool P2, bool NONNEG>
-__global__ void __launch_bounds__(TX* TY, TF_K45_MINB)
+// MB: resident CTAs per SM the registers are budgeted for.  MB = 3 (80 registers,
+// small spills) is ~2 % faster per SM than MB = 2 (128 registers) but each CTA --
+// which walks every plane of its tile column -- runs ~1.47x longer, so it only pays
+// when the tile count fills enough waves (k45_minblocks(); profiles/r02).
+template <bool P2, bool NONNEG, int MB>
+__global__ void __launch_bounds__(TX* TY, MB)
 k_prior_energy_update(Planes F, Planes FP, const float* __restrict__ Kf, const float* Kfp,
                       const float* __restrict__ rstar, float* f_new, double* __restrict__ partial,
                       int nz, int h, int w, float lam, float inv_L, int energy, PriorConsts pc,
@@ -1220,11 +1224,16 @@ int prior_energy_update(const float* f, const float* f_lo, const float* f_hi, co
   const Planes F{f, f_lo, f_hi}, FP{fp, fp_lo, fp_hi};
   const dim3 sgrid = sym_grid(h, w_);
   const size_t smem = sym_smem_bytes(true);
-#define TF_K45(P2V, NN)                                                                      \
-  do {                                                                                       \
-    TF_TRY(prep_kernel(k_prior_energy_update<P2V, NN>, smem));                               \
-    k_prior_energy_update<P2V, NN><<<sgrid, TX * TY, smem, st>>>(                            \
-        F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, lam, inv_L, with_prior, pc, state); \
+  // waves of tile columns at 2 vs 3 CTAs per SM (a 3-CTA wave is ~1.47x longer)
+  const long long tiles = (long long)sgrid.x * sgrid.y, sms = num_sms();
+  const bool mb3 = TF_K45_MB3 && 147 * ((tiles + 3 * sms - 1) / (3 * sms)) <
+                                      100 * ((tiles + 2 * sms - 1) / (2 * sms));
+#define TF_K45(P2V, NN)                                                                        \
+  do {                                                                                         \
+    auto kern = mb3 ? k_prior_energy_update<P2V, NN, 3> : k_prior_energy_update<P2V, NN, 2>;   \
+    TF_TRY(prep_kernel(kern, smem));                                                           \
+    kern<<<sgrid, TX * TY, smem, st>>>(F, FP, Kf, Kfp, rstar, f_new, partial, nz, h, w_, lam,  \
+                                       inv_L, with_prior, pc, state);                          \
   } while (0)
   if (p == 2.0) { if (nonneg) TF_K45(true, true); else TF_K45(true, false); }
   else { if (nonneg) TF_K45(false, true); else TF_K45(false, false); }
